@@ -1,0 +1,219 @@
+/*
+ * vmc.h — C-ABI of the B200 voxel Monte Carlo photon-transport library
+ * (libvoxmc_b200.so). Plain C types only: no torch, no C++ objects.
+ *
+ * This is the drop-in boundary for the reference's per-device executor and
+ * multi-device runner (reference = /root/reference/proj, "voxmc"):
+ *
+ *   vmc_run_range      replaces voxmc::run_group_dynamic
+ *                      (proj/core/include/voxmc/scheduler.hpp:98-99,
+ *                       impl proj/core/src/scheduler.cpp:255-324)
+ *   vmc_run_multi      replaces voxmc::run_multi_device
+ *                      (scheduler.hpp:143-145, scheduler.cpp:395-451)
+ *   vmc_partition      replaces partition_s1/s2/s3 + make_partition
+ *                      (scheduler.hpp:45-56, scheduler.cpp:49-251)
+ *   vmc_rng_kat        exposes RngStream::next_u64 on the device
+ *                      (proj/core/include/voxmc/rng.hpp:11-35, proj/core/src/rng.cpp:5-19)
+ *   vmc_quantum_for    FluenceMap quantum rule (proj/core/src/fluence.cpp:11-14)
+ *   vmc_plan_*         device-resident form of the executor (scene uploaded
+ *                      once, buffers owned by the caller, e.g. torch tensors),
+ *                      used for in-HBM timing and the NCCL reduce path.
+ *
+ * Error convention (all int-returning functions): 0 = ok;
+ * VMC_ERR_VALIDATION (→ voxmc::ValidationError / SourceOutsideDomain in the
+ * C++ shim, reference errors.hpp:9-59); VMC_ERR_RUNTIME (CUDA / NCCL /
+ * allocation). The message of the last failure on the calling thread is
+ * returned by vmc_last_error().
+ *
+ * Fluence cells are signed 64-bit fixed point exactly as the reference's
+ * FluenceMap: value = cell * quantum, quantum = 2^-(62 - bit_width(N))
+ * with N = config.photon_count (the GLOBAL photon count, not the range).
+ * Layout [gate][z][y][x], x fastest (reference VoxelGrid::linear, types.hpp:68-72).
+ */
+#ifndef VMC_H_
+#define VMC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VMC_ABI_VERSION 1
+
+#define VMC_OK 0
+#define VMC_ERR_VALIDATION 1
+#define VMC_ERR_RUNTIME 2
+
+/* boundary_mode (reference BoundaryMode, types.hpp:95) */
+#define VMC_BOUNDARY_TERMINATE 0
+#define VMC_BOUNDARY_REFLECT 1
+
+/* accumulation_mode (reference AccumulationMode, types.hpp:94). Accepted for
+ * API parity; the device always accumulates with exact integer atomics, which
+ * give the same raw cells as either reference mode (fluence.hpp:15-25). */
+#define VMC_ACCUM_SHARED_ATOMIC 0
+#define VMC_ACCUM_PRIVATE_MERGE 1
+
+/* precision: FP32 is the product path; FP64 re-runs the reference's double
+ * arithmetic on the device (parity/diagnostic mode). */
+#define VMC_PRECISION_FP32 0
+#define VMC_PRECISION_FP64 1
+
+/* Labeled voxel volume + media + source (reference VoxelGrid types.hpp:56-92,
+ * OpticalProperties types.hpp:37-44, Source types.hpp:112-116). */
+typedef struct vmc_scene {
+  int32_t nx, ny, nz;
+  double voxel_mm;
+  const uint8_t* labels;  /* nx*ny*nz labels, x fastest; label < nmedia */
+  int32_t nmedia;
+  const double* media;    /* [nmedia][4] = mua (1/mm), mus (1/mm), g, n; [0] = exterior */
+  double src_pos[3];
+  double src_dir[3];
+  int32_t isotropic;
+} vmc_scene;
+
+/* Run parameters (reference SimulationConfig types.hpp:97-108) plus the
+ * B200 build's additions: time gates and disk detectors. */
+typedef struct vmc_config {
+  uint64_t photon_count;       /* global N: fixes the quantum */
+  uint64_t master_seed;
+  int32_t accumulation_mode;   /* VMC_ACCUM_* */
+  int32_t boundary_mode;       /* VMC_BOUNDARY_* */
+  double tmax_ns;              /* photon time horizon */
+  double roulette_threshold;
+  int32_t roulette_multiplier;
+  int32_t workgroup_size;      /* CUDA block size; 0 = library default */
+  int32_t ngates;              /* >= 1; gate g covers [g, g+1) * tmax_ns/ngates */
+  int32_t precision;           /* VMC_PRECISION_* */
+  int32_t ndet;                /* number of disk detectors (0 = none) */
+  int32_t reserved0;
+  const double* det;           /* [ndet][4] = x, y, z, radius (mm) */
+  uint64_t det_capacity;       /* max detector records stored */
+} vmc_config;
+
+/* Terminal weight bookkeeping (reference PhotonDisposition,
+ * transport.hpp:89-102) in the fluence quantum: value = q * quantum. */
+typedef struct vmc_disposition {
+  int64_t deposited_q;
+  int64_t escaped_q;
+  int64_t killed_q;
+  int64_t truncated_q;
+  double quantum;
+} vmc_disposition;
+
+/* Device capacity for partitioning (reference DeviceProfile, scheduler.hpp:21-28). */
+typedef struct vmc_device_profile {
+  int32_t cores;
+  int32_t reserved0;
+  double a;   /* ms per photon */
+  double t0;  /* ms startup overhead */
+} vmc_device_profile;
+
+#define VMC_STRATEGY_S1 1
+#define VMC_STRATEGY_S2 2
+#define VMC_STRATEGY_S3 3
+
+/* Per-photon diagnostic record (tests only; no reference equivalent beyond
+ * simulate_photon_trace, transport.cpp:368-380). Dispositions in launched
+ * weight units; draws = RNG u64 draws consumed by the photon. */
+typedef struct vmc_photon_trace {
+  uint32_t draws;
+  uint32_t steps;
+  uint32_t scatters;
+  uint32_t flags;  /* bit0 escaped, bit1 killed, bit2 truncated, bit3 detected */
+  double deposited;
+  double escaped;
+  double killed;
+  double truncated;
+} vmc_photon_trace;
+
+/* Detector record: fixed header + one float per interior label 1..nmedia-1.
+ *   uint64 photon_index; uint32 det_id; uint32 nscat; float w_exit;
+ *   float t_exit_ns; float ppath_mm[nmedia-1]; (padded to 8 bytes)
+ * Records returned by vmc_run_range / vmc_run_multi are sorted by
+ * photon_index, so output is identical for any GPU count. */
+typedef struct vmc_det_record_head {
+  uint64_t photon_index;
+  uint32_t det_id;
+  uint32_t nscat;
+  float w_exit;
+  float t_exit_ns;
+} vmc_det_record_head;
+
+size_t vmc_det_record_bytes(int32_t nmedia);
+
+int vmc_abi_version(void);
+const char* vmc_last_error(void);
+int vmc_device_count(void);
+
+/* Quantum for N photons: 2^-(62 - bit_width(N|1)) (fluence.cpp:11-14). */
+double vmc_quantum_for(uint64_t photon_count);
+
+/* Validates a scene/config pair exactly as the reference does
+ * (VoxelGrid ctor types.cpp:7-33, SimulationConfig::validate types.cpp:44-52,
+ * launch voxel check transport.cpp:96-99). */
+int vmc_validate(const vmc_scene* scene, const vmc_config* config);
+
+/* Per-device executor, host buffers (the reference-facing call).
+ * Simulates global photons [first_index, first_index+count) on CUDA device
+ * `device`; photon k uses RNG stream (master_seed, k).
+ * cells_out: host [ngates*nx*ny*nz] int64, overwritten (may be NULL).
+ * totals_out: may be NULL. det_out: host buffer of det_capacity records
+ * (may be NULL when ndet == 0); det_count_out = records detected (may exceed
+ * det_capacity; only min(count, capacity) are stored).
+ * wall_ms_out: device time of the run (events around the kernels). */
+int vmc_run_range(const vmc_scene* scene, const vmc_config* config, uint64_t first_index,
+                  uint64_t count, int device, int64_t* cells_out, vmc_disposition* totals_out,
+                  void* det_out, uint64_t* det_count_out, double* wall_ms_out);
+
+/* Multi-device runner inside one process: contiguous ranges counts[i] in
+ * device order starting at photon 0 (reference scheduler.cpp:405-413), one
+ * host thread per device, exact int64 sum of the per-device maps (NCCL
+ * reduce to devices[0] when ndev > 1). per_device_ms: [ndev] (may be NULL). */
+int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, const int* devices,
+                  const uint64_t* counts, int64_t* cells_out, vmc_disposition* totals_out,
+                  void* det_out, uint64_t* det_count_out, double* per_device_ms,
+                  double* reduce_ms);
+
+/* Photon-count partition over devices (reference partition_s1/s2/s3). */
+int vmc_partition(int strategy, uint64_t total, int ndev, const vmc_device_profile* devices,
+                  uint64_t* counts_out);
+double vmc_model_makespan(int ndev, const uint64_t* counts, const vmc_device_profile* devices);
+
+/* First n outputs of RngStream(seed, stream_id).next_u64() computed on the device. */
+int vmc_rng_kat(uint64_t seed, uint64_t stream_id, int n, int device, uint64_t* out);
+
+/* ---- device-resident plan: scene on the GPU, caller-owned buffers ------- */
+typedef struct vmc_plan vmc_plan;
+
+int vmc_plan_create(const vmc_scene* scene, const vmc_config* config, int device,
+                    vmc_plan** out);
+int vmc_plan_destroy(vmc_plan* plan);
+/* Number of int64 cells (ngates*nx*ny*nz) and the record stride. */
+uint64_t vmc_plan_cell_count(const vmc_plan* plan);
+
+#define VMC_RUN_ZERO 1u /* zero d_cells / d_totals / d_det_count before the run */
+
+/* Runs photons [first_index, first_index+count) on `stream` (cudaStream_t, 0 =
+ * legacy default). Device buffers: d_cells [cell_count] int64 (accumulated),
+ * d_totals [4] int64 (deposited/escaped/killed/truncated quanta, accumulated),
+ * d_det (det_capacity records) and d_det_count [1] uint64 (may be NULL when
+ * ndet == 0). Asynchronous: returns after enqueueing. */
+int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, int64_t* d_cells,
+                 int64_t* d_totals, void* d_det, uint64_t* d_det_count, void* stream,
+                 uint32_t flags);
+
+/* Per-photon diagnostics for photons [first_index, first_index+count) into the
+ * host array out[count]. Deposits are not accumulated. Synchronous. */
+int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_photon_trace* out);
+
+/* Number of kernels vmc_plan_run enqueues per call (for launch accounting). */
+int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VMC_H_ */
