@@ -42,6 +42,12 @@ extern "C" {
 
 #define VMC_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define VMC_API __attribute__((visibility("default")))
+#else
+#define VMC_API
+#endif
+
 #define VMC_OK 0
 #define VMC_ERR_VALIDATION 1
 #define VMC_ERR_RUNTIME 2
@@ -142,19 +148,19 @@ typedef struct vmc_det_record_head {
   float t_exit_ns;
 } vmc_det_record_head;
 
-size_t vmc_det_record_bytes(int32_t nmedia);
+VMC_API size_t vmc_det_record_bytes(int32_t nmedia);
 
-int vmc_abi_version(void);
-const char* vmc_last_error(void);
-int vmc_device_count(void);
+VMC_API int vmc_abi_version(void);
+VMC_API const char* vmc_last_error(void);
+VMC_API int vmc_device_count(void);
 
 /* Quantum for N photons: 2^-(62 - bit_width(N|1)) (fluence.cpp:11-14). */
-double vmc_quantum_for(uint64_t photon_count);
+VMC_API double vmc_quantum_for(uint64_t photon_count);
 
 /* Validates a scene/config pair exactly as the reference does
  * (VoxelGrid ctor types.cpp:7-33, SimulationConfig::validate types.cpp:44-52,
  * launch voxel check transport.cpp:96-99). */
-int vmc_validate(const vmc_scene* scene, const vmc_config* config);
+VMC_API int vmc_validate(const vmc_scene* scene, const vmc_config* config);
 
 /* Per-device executor, host buffers (the reference-facing call).
  * Simulates global photons [first_index, first_index+count) on CUDA device
@@ -164,7 +170,7 @@ int vmc_validate(const vmc_scene* scene, const vmc_config* config);
  * (may be NULL when ndet == 0); det_count_out = records detected (may exceed
  * det_capacity; only min(count, capacity) are stored).
  * wall_ms_out: device time of the run (events around the kernels). */
-int vmc_run_range(const vmc_scene* scene, const vmc_config* config, uint64_t first_index,
+VMC_API int vmc_run_range(const vmc_scene* scene, const vmc_config* config, uint64_t first_index,
                   uint64_t count, int device, int64_t* cells_out, vmc_disposition* totals_out,
                   void* det_out, uint64_t* det_count_out, double* wall_ms_out);
 
@@ -172,27 +178,27 @@ int vmc_run_range(const vmc_scene* scene, const vmc_config* config, uint64_t fir
  * device order starting at photon 0 (reference scheduler.cpp:405-413), one
  * host thread per device, exact int64 sum of the per-device maps (NCCL
  * reduce to devices[0] when ndev > 1). per_device_ms: [ndev] (may be NULL). */
-int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, const int* devices,
+VMC_API int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, const int* devices,
                   const uint64_t* counts, int64_t* cells_out, vmc_disposition* totals_out,
                   void* det_out, uint64_t* det_count_out, double* per_device_ms,
                   double* reduce_ms);
 
 /* Photon-count partition over devices (reference partition_s1/s2/s3). */
-int vmc_partition(int strategy, uint64_t total, int ndev, const vmc_device_profile* devices,
+VMC_API int vmc_partition(int strategy, uint64_t total, int ndev, const vmc_device_profile* devices,
                   uint64_t* counts_out);
-double vmc_model_makespan(int ndev, const uint64_t* counts, const vmc_device_profile* devices);
+VMC_API double vmc_model_makespan(int ndev, const uint64_t* counts, const vmc_device_profile* devices);
 
 /* First n outputs of RngStream(seed, stream_id).next_u64() computed on the device. */
-int vmc_rng_kat(uint64_t seed, uint64_t stream_id, int n, int device, uint64_t* out);
+VMC_API int vmc_rng_kat(uint64_t seed, uint64_t stream_id, int n, int device, uint64_t* out);
 
 /* ---- device-resident plan: scene on the GPU, caller-owned buffers ------- */
 typedef struct vmc_plan vmc_plan;
 
-int vmc_plan_create(const vmc_scene* scene, const vmc_config* config, int device,
+VMC_API int vmc_plan_create(const vmc_scene* scene, const vmc_config* config, int device,
                     vmc_plan** out);
-int vmc_plan_destroy(vmc_plan* plan);
+VMC_API int vmc_plan_destroy(vmc_plan* plan);
 /* Number of int64 cells (ngates*nx*ny*nz) and the record stride. */
-uint64_t vmc_plan_cell_count(const vmc_plan* plan);
+VMC_API uint64_t vmc_plan_cell_count(const vmc_plan* plan);
 
 #define VMC_RUN_ZERO 1u /* zero d_cells / d_totals / d_det_count before the run */
 
@@ -201,16 +207,16 @@ uint64_t vmc_plan_cell_count(const vmc_plan* plan);
  * d_totals [4] int64 (deposited/escaped/killed/truncated quanta, accumulated),
  * d_det (det_capacity records) and d_det_count [1] uint64 (may be NULL when
  * ndet == 0). Asynchronous: returns after enqueueing. */
-int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, int64_t* d_cells,
+VMC_API int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, int64_t* d_cells,
                  int64_t* d_totals, void* d_det, uint64_t* d_det_count, void* stream,
                  uint32_t flags);
 
 /* Per-photon diagnostics for photons [first_index, first_index+count) into the
  * host array out[count]. Deposits are not accumulated. Synchronous. */
-int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_photon_trace* out);
+VMC_API int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_photon_trace* out);
 
 /* Number of kernels vmc_plan_run enqueues per call (for launch accounting). */
-int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags);
+VMC_API int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,75 @@
+"""Build of the native library libvoxmc_b200.so (sm_100a), in-tree.
+
+nvcc -gencode arch=compute_100a,code=sm_100a for every .cu; the FP64 parity
+instantiation of K1 is compiled with --fmad=false. Output:
+paper_1711_03244_b200/lib/libvoxmc_b200.so (git-ignored, travels with gpurun).
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT_DIR = os.path.join(PKG, "lib")
+OBJ_DIR = os.path.join(PKG, "lib", "obj")
+LIB = os.path.join(OUT_DIR, "libvoxmc_b200.so")
+
+NVCC = os.environ.get("NVCC", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+# (source, object, extra flags)
+UNITS = [
+    ("transport_kernels.cu", "transport_f32.o", ["-DVMC_REAL=float"]),
+    ("transport_kernels.cu", "transport_f64.o", ["-DVMC_REAL=double", "--fmad=false"]),
+    ("capi.cu", "capi.o", []),
+    ("partition.cpp", "partition.o", []),
+    ("voxmc_api.cpp", "voxmc_api.o", []),
+]
+
+HEADERS = ["transport.cuh", "rng.cuh", "partition.hpp"]
+
+
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "vmc.h")]
+    deps += [os.path.join(ROOT, "include", "voxmc", f) for f in os.listdir(os.path.join(ROOT, "include", "voxmc"))]
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _compile(src: str, obj: str, extra, verbose: bool) -> None:
+    srcp = os.path.join(CSRC, src)
+    objp = os.path.join(OBJ_DIR, obj)
+    if not _stale(objp, srcp):
+        return
+    lang = [] if src.endswith(".cu") else ["-x", "cu"] if False else []
+    cmd = [NVCC] + ARCH + COMMON + extra + lang + ["-c", srcp, "-o", objp]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    units = [u for u in UNITS if os.path.exists(os.path.join(CSRC, u[0]))]
+    with cf.ThreadPoolExecutor(max_workers=len(units)) as ex:
+        for f in [ex.submit(_compile, s, o, e, verbose) for s, o, e in units]:
+            f.result()
+    objs = [os.path.join(OBJ_DIR, o) for _, o, _ in units]
+    if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", LIB] + objs + ["-ldl", "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

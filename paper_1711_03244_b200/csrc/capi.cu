@@ -1,0 +1,802 @@
+// capi.cu — implementation of the C-ABI in include/vmc.h.
+//
+// Host-side executor for one B200: validates the scene exactly as the
+// reference does, stages labels (packed uint8) and the media table in HBM,
+// sizes a persistent grid by occupancy, and launches K1. The synchronous
+// entry points (vmc_run_range / vmc_run_multi) are the drop-in for
+// run_group_dynamic / run_multi_device (proj/core/src/scheduler.cpp:255-451).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/vmc.h"
+#include "partition.hpp"
+#include "transport.cuh"
+
+namespace vmc {
+const void* transport_kernel_float(bool gates, bool det, bool trace);
+const void* transport_kernel_double(bool gates, bool det, bool trace);
+}  // namespace vmc
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct VmcError : std::runtime_error {
+  int code;
+  VmcError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail_validation(const std::string& m) { throw VmcError(VMC_ERR_VALIDATION, m); }
+[[noreturn]] void fail_runtime(const std::string& m) { throw VmcError(VMC_ERR_RUNTIME, m); }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail_runtime(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VMC_OK;
+  } catch (const VmcError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const vmc::PartitionError& e) {
+    g_last_error = e.what();
+    return VMC_ERR_VALIDATION;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return VMC_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return VMC_ERR_RUNTIME;
+  }
+}
+
+int bit_width_u64(uint64_t v) {
+  int w = 0;
+  while (v) {
+    ++w;
+    v >>= 1;
+  }
+  return w;
+}
+
+// FluenceMap quantum rule (proj/core/src/fluence.cpp:11-14): power-of-two
+// quantum so N unit-weight photons cannot overflow 63 bits.
+int quantum_bits(uint64_t n) { return 62 - bit_width_u64(n | 1u); }
+
+struct HostLaunch {
+  double dir[3];
+  double pos[3];
+  int v[3];
+};
+
+// Pencil launch geometry in double on the host (transport.cpp:83-106,
+// VoxelGrid::voxel_of types.cpp:35-42); throws like SourceOutsideDomain.
+HostLaunch pencil_launch(const vmc_scene* s) {
+  HostLaunch L;
+  const double n = std::sqrt(s->src_dir[0] * s->src_dir[0] + s->src_dir[1] * s->src_dir[1] +
+                             s->src_dir[2] * s->src_dir[2]);
+  const double inv = 1.0 / n;
+  for (int k = 0; k < 3; ++k) {
+    L.dir[k] = s->src_dir[k] * inv;
+    L.pos[k] = s->src_pos[k] + L.dir[k] * 1e-6;
+    L.v[k] = static_cast<int>(std::floor(L.pos[k] / s->voxel_mm));
+  }
+  return L;
+}
+
+bool inside(const vmc_scene* s, const int* v) {
+  return v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[0] < s->nx && v[1] < s->ny && v[2] < s->nz;
+}
+
+void validate(const vmc_scene* s, const vmc_config* c) {
+  if (!s || !c) fail_validation("null scene/config");
+  // VoxelGrid ctor, types.cpp:7-33
+  if (s->nx < 1 || s->ny < 1 || s->nz < 1) fail_validation("VoxelGrid: all dims must be >= 1");
+  if (!(s->voxel_mm > 0.0)) fail_validation("VoxelGrid: voxel_size must be > 0");
+  if (s->nmedia < 1 || !s->media) fail_validation("VoxelGrid: media list is empty");
+  if (s->nmedia > 256) fail_validation("VoxelGrid: at most 256 media (uint8 labels)");
+  if (!s->labels) fail_validation("VoxelGrid: label array size does not match dims");
+  for (int m = 0; m < s->nmedia; ++m) {
+    const double* p = s->media + 4 * m;
+    if (p[0] < 0.0 || p[1] < 0.0 || p[2] < -1.0 || p[2] > 1.0 || p[3] < 1.0 || std::isnan(p[0]) ||
+        std::isnan(p[1]) || std::isnan(p[2]) || std::isnan(p[3]))
+      fail_validation("VoxelGrid: invalid optical properties");
+  }
+  const size_t nvox = static_cast<size_t>(s->nx) * s->ny * s->nz;
+  uint8_t mx = 0;
+  for (size_t i = 0; i < nvox; ++i) mx = std::max(mx, s->labels[i]);
+  if (mx >= s->nmedia) fail_validation("VoxelGrid: label exceeds media list");
+  // SimulationConfig::validate, types.cpp:44-52
+  if (c->photon_count < 1) fail_validation("photon_count must be >= 1");
+  if (!(c->tmax_ns > 0.0)) fail_validation("tmax must be > 0");
+  if (!(c->roulette_threshold > 0.0 && c->roulette_threshold < 1.0))
+    fail_validation("roulette_threshold must be in (0, 1)");
+  if (c->roulette_multiplier < 2) fail_validation("roulette_multiplier must be >= 2");
+  if (c->workgroup_size < 0) fail_validation("workgroup_size must be >= 1");
+  // B200 additions
+  if (c->ngates < 1) fail_validation("ngates must be >= 1");
+  if (c->precision != VMC_PRECISION_FP32 && c->precision != VMC_PRECISION_FP64)
+    fail_validation("precision must be VMC_PRECISION_FP32 or VMC_PRECISION_FP64");
+  if (c->boundary_mode != VMC_BOUNDARY_TERMINATE && c->boundary_mode != VMC_BOUNDARY_REFLECT)
+    fail_validation("boundary must be 'terminate' or 'reflect'");
+  if (c->ndet < 0 || c->ndet > vmc::kMaxDet) fail_validation("ndet must be in [0, 16]");
+  if (c->ndet > 0) {
+    if (!c->det) fail_validation("detector array is null");
+    if (s->nmedia - 1 > vmc::kMaxDetMedia) fail_validation("detectors support at most 8 interior media");
+    for (int k = 0; k < c->ndet; ++k)
+      if (!(c->det[4 * k + 3] > 0.0)) fail_validation("detector radius must be > 0");
+  }
+  if (static_cast<unsigned long long>(nvox) * static_cast<unsigned>(c->ngates) > (1ull << 40))
+    fail_validation("volume x gates too large");
+  // launch point (transport.cpp:95-99)
+  if (!s->isotropic) {
+    const double n2 = s->src_dir[0] * s->src_dir[0] + s->src_dir[1] * s->src_dir[1] + s->src_dir[2] * s->src_dir[2];
+    if (!(n2 > 0.0)) fail_validation("source direction must be nonzero");
+    const HostLaunch L = pencil_launch(s);
+    if (!inside(s, L.v)) throw VmcError(VMC_ERR_VALIDATION, "source entry point maps outside the voxel grid");
+  } else {
+    // every launch direction must keep the nudged point inside the grid
+    for (int corner = 0; corner < 8; ++corner) {
+      int v[3];
+      for (int k = 0; k < 3; ++k) {
+        const double p = s->src_pos[k] + ((corner >> k) & 1 ? 1e-6 : -1e-6);
+        v[k] = static_cast<int>(std::floor(p / s->voxel_mm));
+      }
+      if (!inside(s, v)) fail_validation("source entry point maps outside the voxel grid");
+    }
+  }
+}
+
+template <typename Real>
+std::vector<vmc::Medium<Real>> build_media(const vmc_scene* s) {
+  std::vector<vmc::Medium<Real>> out(static_cast<size_t>(s->nmedia));
+  for (int m = 0; m < s->nmedia; ++m) {
+    const double mua = s->media[4 * m], mus = s->media[4 * m + 1], g = s->media[4 * m + 2],
+                 n = s->media[4 * m + 3];
+    vmc::Medium<Real>& M = out[m];
+    std::memset(&M, 0, sizeof M);
+    M.mua = static_cast<Real>(mua);
+    M.mus = static_cast<Real>(mus);
+    M.inv_mus = mus > 0.0 ? static_cast<Real>(1.0 / mus) : Real(0);
+    const double nspm = n * (1.0 / vmc::kLightMmPerNs);  // advance(), transport.cpp:169
+    M.ns_per_mm = static_cast<Real>(nspm);
+    M.mm_per_ns = static_cast<Real>(1.0 / nspm);
+    M.n = static_cast<Real>(n);
+    M.g = static_cast<Real>(g);
+    M.iso = std::fabs(g) < 1e-6 ? 1 : 0;  // hg_cos_theta, transport.cpp:121
+    if (!M.iso) {
+      M.hg_a = static_cast<Real>((1.0 + g * g) / (2.0 * g));
+      M.hg_b = static_cast<Real>(1.0 / (2.0 * g));
+      M.hg_c = static_cast<Real>(1.0 - g * g);
+      M.hg_d = static_cast<Real>(1.0 - g);
+      M.hg_e = static_cast<Real>(2.0 * g);
+    }
+    // refractive-index class: exact double comparison of n (transport.cpp:218, 242)
+    M.nclass = m;
+    for (int j = 0; j < m; ++j)
+      if (s->media[4 * j + 3] == n) {
+        M.nclass = out[j].nclass;
+        break;
+      }
+  }
+  return out;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  int dev = -1;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (dev >= 0 && cur != dev) cudaSetDevice(dev);
+      cudaFree(p);
+      if (dev >= 0 && cur >= 0 && cur != dev) cudaSetDevice(cur);
+    }
+  }
+  void alloc(size_t bytes, int device) {
+    dev = device;
+    ck(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+  }
+};
+
+}  // namespace
+
+struct vmc_plan {
+  int device = 0;
+  vmc_config cfg{};
+  int nx = 0, ny = 0, nz = 0, nmedia = 0;
+  uint64_t ncells = 0;
+  size_t rec_stride = 0;
+  DevBuf labels, media, claim, err;
+  vmc::KernelArgs args{};
+  int sms = 0;
+  int block = vmc::kBlock;
+  size_t smem = 0;
+  int grid = 0, grid_trace = 0;
+  const void* kern = nullptr;
+  const void* kern_trace = nullptr;
+};
+
+namespace {
+
+void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device) {
+  validate(s, c);
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) fail_validation("device index out of range");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  P->device = device;
+  P->cfg = *c;
+  P->cfg.det = nullptr;
+  P->nx = s->nx;
+  P->ny = s->ny;
+  P->nz = s->nz;
+  P->nmedia = s->nmedia;
+  const size_t nvox = static_cast<size_t>(s->nx) * s->ny * s->nz;
+  P->ncells = static_cast<uint64_t>(nvox) * static_cast<uint64_t>(c->ngates);
+  P->rec_stride = vmc_det_record_bytes(s->nmedia);
+
+  P->labels.alloc(nvox, device);
+  ck(cudaMemcpy(P->labels.p, s->labels, nvox, cudaMemcpyHostToDevice), "upload labels");
+  const bool f64 = c->precision == VMC_PRECISION_FP64;
+  size_t media_bytes;
+  if (f64) {
+    auto m = build_media<double>(s);
+    media_bytes = m.size() * sizeof(m[0]);
+    P->media.alloc(media_bytes, device);
+    ck(cudaMemcpy(P->media.p, m.data(), media_bytes, cudaMemcpyHostToDevice), "upload media");
+  } else {
+    auto m = build_media<float>(s);
+    media_bytes = m.size() * sizeof(m[0]);
+    P->media.alloc(media_bytes, device);
+    ck(cudaMemcpy(P->media.p, m.data(), media_bytes, cudaMemcpyHostToDevice), "upload media");
+  }
+  P->claim.alloc(sizeof(unsigned long long), device);
+  P->err.alloc(sizeof(int), device);
+  ck(cudaMemset(P->err.p, 0, sizeof(int)), "cudaMemset");
+
+  vmc::KernelArgs& A = P->args;
+  std::memset(&A, 0, sizeof A);
+  A.labels = static_cast<const uint8_t*>(P->labels.p);
+  A.nx = s->nx;
+  A.ny = s->ny;
+  A.nz = s->nz;
+  A.nxy = static_cast<long long>(s->nx) * s->ny;
+  A.nvox = static_cast<long long>(nvox);
+  A.h = s->voxel_mm;
+  A.nmedia = s->nmedia;
+  A.iso_source = s->isotropic ? 1 : 0;
+  A.media = P->media.p;
+  for (int k = 0; k < 3; ++k) A.src_pos[k] = s->src_pos[k];
+  int center[3];
+  if (!s->isotropic) {
+    const HostLaunch L = pencil_launch(s);
+    for (int k = 0; k < 3; ++k) {
+      A.dir0[k] = L.dir[k];
+      A.pos0[k] = L.pos[k];
+      A.v0[k] = L.v[k];
+      center[k] = L.v[k] + static_cast<int>(std::lround(L.dir[k] * 7.0));
+    }
+    A.lab0 = s->labels[static_cast<size_t>(L.v[0]) + static_cast<size_t>(s->nx) * (L.v[1] + static_cast<size_t>(s->ny) * L.v[2])];
+  } else {
+    for (int k = 0; k < 3; ++k) center[k] = static_cast<int>(std::floor(s->src_pos[k] / s->voxel_mm));
+  }
+  A.seed = c->master_seed;
+  A.tmax = c->tmax_ns;
+  A.rthr = c->roulette_threshold;
+  A.rmult = c->roulette_multiplier;
+  A.inv_rmult = 1.0 / c->roulette_multiplier;  // roulette(), transport.cpp:301
+  A.reflect = c->boundary_mode == VMC_BOUNDARY_REFLECT ? 1 : 0;
+  A.ngates = c->ngates;
+  A.inv_gate_w = static_cast<double>(c->ngates) / c->tmax_ns;
+  A.qscale = std::ldexp(1.0, quantum_bits(c->photon_count));
+  A.claim = static_cast<unsigned long long*>(P->claim.p);
+  A.error_flag = static_cast<int*>(P->err.p);
+
+  // hot box: up to 16^3 cells per gate within a 32 KB (lo/hi u32) budget,
+  // placed around the launch voxel and pushed along the launch direction.
+  {
+    const int dims[3] = {s->nx, s->ny, s->nz};
+    int side = 16;
+    while (side > 1 && static_cast<long long>(side) * side * side * c->ngates * 8 > 32 * 1024) --side;
+    int n[3], o[3];
+    for (int k = 0; k < 3; ++k) {
+      n[k] = std::min(side, dims[k]);
+      o[k] = center[k] - n[k] / 2;
+      o[k] = std::max(0, std::min(o[k], dims[k] - n[k]));
+    }
+    A.bx0 = o[0];
+    A.by0 = o[1];
+    A.bz0 = o[2];
+    A.bnx = n[0];
+    A.bny = n[1];
+    A.bnz = n[2];
+    A.box_cells = side >= 4 ? n[0] * n[1] * n[2] * c->ngates : 0;
+  }
+  A.ndet = c->ndet;
+  A.nppath = std::max(0, s->nmedia - 1);
+  A.rec_stride = static_cast<int>(P->rec_stride);
+  for (int k = 0; k < c->ndet; ++k)
+    for (int j = 0; j < 4; ++j) A.det[k][j] = c->det[4 * k + j];
+  A.det_cap = c->det_capacity;
+
+  const bool gates = c->ngates > 1, det = c->ndet > 0;
+  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
+  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
+  P->smem = media_bytes + static_cast<size_t>(A.box_cells) * 8;
+  ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  if (P->smem > 48 * 1024) {
+    ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+    ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+  }
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern, P->block, P->smem), "occupancy");
+  P->grid = std::max(1, per_sm) * P->sms;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern_trace, P->block, P->smem), "occupancy");
+  P->grid_trace = std::max(1, per_sm) * P->sms;
+}
+
+void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells, int64_t* d_totals,
+                  void* d_det, uint64_t* d_det_count, cudaStream_t st, uint32_t flags, bool trace,
+                  vmc_photon_trace* d_trace) {
+  if (!d_cells || !d_totals) fail_validation("device cells/totals buffers are required");
+  if (P->cfg.ndet > 0 && P->cfg.det_capacity > 0 && !d_det) fail_validation("detector buffer is required");
+  if (P->cfg.ndet > 0 && !d_det_count) fail_validation("detector count buffer is required");
+  if (first + count < first) fail_validation("photon range overflows");
+  ck(cudaSetDevice(P->device), "cudaSetDevice");
+  if (flags & VMC_RUN_ZERO) {
+    ck(cudaMemsetAsync(d_cells, 0, P->ncells * sizeof(int64_t), st), "zero cells");
+    ck(cudaMemsetAsync(d_totals, 0, 4 * sizeof(int64_t), st), "zero totals");
+    if (d_det_count) ck(cudaMemsetAsync(d_det_count, 0, sizeof(uint64_t), st), "zero det count");
+  }
+  if (count == 0) return;
+  ck(cudaMemsetAsync(P->claim.p, 0, sizeof(unsigned long long), st), "zero claim");
+  vmc::KernelArgs A = P->args;
+  A.first = first;
+  A.count = count;
+  A.cells = reinterpret_cast<long long*>(d_cells);
+  A.totals = reinterpret_cast<long long*>(d_totals);
+  A.det_out = static_cast<unsigned char*>(d_det);
+  A.det_count = reinterpret_cast<unsigned long long*>(d_det_count);
+  A.trace = d_trace;
+  void* argv[] = {&A};
+  // never launch more persistent threads than photons need
+  const uint64_t need_blocks = (count + P->block - 1) / P->block;
+  const int full = trace ? P->grid_trace : P->grid;
+  const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));
+  ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv, P->smem, st),
+     "launch transport");
+}
+
+void check_launch_errors(vmc_plan* P) {
+  int h = 0;
+  ck(cudaMemcpy(&h, P->err.p, sizeof(int), cudaMemcpyDeviceToHost), "read error flag");
+  if (h) {
+    cudaMemset(P->err.p, 0, sizeof(int));
+    fail_validation("source entry point maps outside the voxel grid");
+  }
+}
+
+// Sort packed detector records by photon index (deterministic output for any
+// device count / claim order).
+void sort_records(unsigned char* recs, uint64_t n, size_t stride) {
+  if (n < 2) return;
+  std::vector<uint64_t> order(n);
+  std::iota(order.begin(), order.end(), uint64_t{0});
+  auto key = [&](uint64_t i) {
+    uint64_t k;
+    std::memcpy(&k, recs + i * stride, sizeof k);
+    return k;
+  };
+  std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return key(a) < key(b); });
+  std::vector<unsigned char> tmp(n * stride);
+  for (uint64_t i = 0; i < n; ++i) std::memcpy(tmp.data() + i * stride, recs + order[i] * stride, stride);
+  std::memcpy(recs, tmp.data(), n * stride);
+}
+
+// ---- one device, host buffers ---------------------------------------------
+struct RangeResult {
+  std::vector<int64_t> cells;
+  int64_t totals[4] = {0, 0, 0, 0};
+  std::vector<unsigned char> det;
+  uint64_t det_count = 0;
+  double ms = 0.0;
+};
+
+void run_range_device(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count, int device,
+                      int64_t* cells_out, int64_t* totals_out, unsigned char* det_out, uint64_t* det_count_out,
+                      double* ms_out) {
+  vmc_plan P;
+  plan_init(&P, s, c, device);
+  DevBuf cells, totals, det, detn;
+  cells.alloc(P.ncells * sizeof(int64_t), device);
+  totals.alloc(4 * sizeof(int64_t), device);
+  const uint64_t cap = c->ndet > 0 ? c->det_capacity : 0;
+  det.alloc(cap * P.rec_stride, device);
+  detn.alloc(sizeof(uint64_t), device);
+  cudaStream_t st;
+  ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  try {
+    ck(cudaEventRecord(e0, st), "event record");
+    plan_enqueue(&P, first, count, static_cast<int64_t*>(cells.p), static_cast<int64_t*>(totals.p), det.p,
+                 static_cast<uint64_t*>(detn.p), st, VMC_RUN_ZERO, false, nullptr);
+    ck(cudaEventRecord(e1, st), "event record");
+    if (cells_out)
+      ck(cudaMemcpyAsync(cells_out, cells.p, P.ncells * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "download");
+    if (totals_out) ck(cudaMemcpyAsync(totals_out, totals.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "download");
+    uint64_t n = 0;
+    ck(cudaMemcpyAsync(&n, detn.p, sizeof n, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "run");
+    if (c->ndet > 0) {
+      const uint64_t keep = std::min(n, cap);
+      if (det_out && keep) {
+        ck(cudaMemcpy(det_out, det.p, keep * P.rec_stride, cudaMemcpyDeviceToHost), "download det");
+        sort_records(det_out, keep, P.rec_stride);
+      }
+    }
+    if (det_count_out) *det_count_out = c->ndet > 0 ? n : 0;
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    if (ms_out) *ms_out = ms;
+    check_launch_errors(&P);
+  } catch (...) {
+    cudaStreamDestroy(st);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  cudaStreamDestroy(st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// ---- NCCL, loaded on demand (only vmc_run_multi with ndev > 1 needs it) ----
+struct Nccl {
+  void* h = nullptr;
+  int (*CommInitAll)(void** comms, int ndev, const int* devlist) = nullptr;
+  int (*CommDestroy)(void* comm) = nullptr;
+  int (*Reduce)(const void*, void*, size_t, int, int, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (n.h) break;
+    }
+    if (!n.h) return;
+    n.CommInitAll = reinterpret_cast<decltype(n.CommInitAll)>(dlsym(n.h, "ncclCommInitAll"));
+    n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(n.h, "ncclCommDestroy"));
+    n.Reduce = reinterpret_cast<decltype(n.Reduce)>(dlsym(n.h, "ncclReduce"));
+    n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(n.h, "ncclGroupStart"));
+    n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(n.h, "ncclGroupEnd"));
+    n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(n.h, "ncclGetErrorString"));
+  });
+  if (!n.h || !n.CommInitAll || !n.Reduce || !n.GroupStart || !n.GroupEnd)
+    fail_runtime("NCCL (libnccl.so.2) is required for multi-GPU runs and could not be loaded");
+  return n;
+}
+
+void nck(int r, const char* what) {
+  if (r != 0) {
+    Nccl& n = nccl();
+    fail_runtime(std::string(what) + ": " + (n.GetErrorString ? n.GetErrorString(r) : "nccl error"));
+  }
+}
+
+constexpr int kNcclInt64 = 4;  // ncclInt64
+constexpr int kNcclSum = 0;    // ncclSum
+
+}  // namespace
+
+namespace {
+__global__ void k_rng_kat(uint64_t seed, uint64_t stream, int n, uint64_t* out) {
+  vmc::Xs128p<false> r;
+  r.seed(seed, stream);
+  for (int i = 0; i < n; ++i) out[i] = r.next();
+}
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int vmc_rng_kat(uint64_t seed, uint64_t stream_id, int n, int device, uint64_t* out) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !out)) fail_validation("rng_kat: bad output");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    DevBuf d;
+    d.alloc(static_cast<size_t>(n) * sizeof(uint64_t), device);
+    k_rng_kat<<<1, 1>>>(seed, stream_id, n, static_cast<uint64_t*>(d.p));
+    ck(cudaGetLastError(), "launch rng_kat");
+    ck(cudaMemcpy(out, d.p, static_cast<size_t>(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost), "download");
+  });
+}
+
+size_t vmc_det_record_bytes(int32_t nmedia) {
+  const size_t raw = sizeof(vmc_det_record_head) + sizeof(float) * static_cast<size_t>(nmedia > 1 ? nmedia - 1 : 0);
+  return (raw + 7) & ~static_cast<size_t>(7);
+}
+
+int vmc_abi_version(void) { return VMC_ABI_VERSION; }
+
+const char* vmc_last_error(void) { return g_last_error.c_str(); }
+
+int vmc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+double vmc_quantum_for(uint64_t photon_count) { return std::ldexp(1.0, -quantum_bits(photon_count)); }
+
+int vmc_validate(const vmc_scene* scene, const vmc_config* config) {
+  return guarded([&] { validate(scene, config); });
+}
+
+int vmc_run_range(const vmc_scene* scene, const vmc_config* config, uint64_t first_index, uint64_t count,
+                  int device, int64_t* cells_out, vmc_disposition* totals_out, void* det_out,
+                  uint64_t* det_count_out, double* wall_ms_out) {
+  return guarded([&] {
+    int64_t tot[4] = {0, 0, 0, 0};
+    run_range_device(scene, config, first_index, count, device, cells_out, tot,
+                     static_cast<unsigned char*>(det_out), det_count_out, wall_ms_out);
+    if (totals_out) {
+      totals_out->deposited_q = tot[0];
+      totals_out->escaped_q = tot[1];
+      totals_out->killed_q = tot[2];
+      totals_out->truncated_q = tot[3];
+      totals_out->quantum = vmc_quantum_for(config->photon_count);
+    }
+  });
+}
+
+int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, const int* devices,
+                  const uint64_t* counts, int64_t* cells_out, vmc_disposition* totals_out, void* det_out,
+                  uint64_t* det_count_out, double* per_device_ms, double* reduce_ms) {
+  return guarded([&] {
+    validate(scene, config);
+    if (ndev < 1 || !devices || !counts) fail_validation("run_multi: no devices");
+    std::vector<uint64_t> first(ndev);
+    uint64_t next = 0;  // contiguous ranges in device order (scheduler.cpp:405-410)
+    for (int i = 0; i < ndev; ++i) {
+      first[i] = next;
+      next += counts[i];
+    }
+    const size_t stride = vmc_det_record_bytes(scene->nmedia);
+    const uint64_t cap = config->ndet > 0 ? config->det_capacity : 0;
+
+    struct Slot {
+      std::unique_ptr<vmc_plan> plan;
+      DevBuf cells, totals, det, detn;
+      cudaStream_t st = nullptr;
+      double ms = 0.0;
+      uint64_t ndet = 0;
+      std::string err;
+      int code = 0;
+    };
+    std::vector<Slot> slot(ndev);
+    auto worker = [&](int i) {
+      Slot& S = slot[i];
+      S.code = guarded([&] {
+        const int dev = devices[i];
+        S.plan.reset(new vmc_plan);
+        plan_init(S.plan.get(), scene, config, dev);
+        S.cells.alloc(S.plan->ncells * sizeof(int64_t), dev);
+        S.totals.alloc(4 * sizeof(int64_t), dev);
+        S.det.alloc(cap * stride, dev);
+        S.detn.alloc(sizeof(uint64_t), dev);
+        ck(cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking), "stream");
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventRecord(e0, S.st), "event");
+        plan_enqueue(S.plan.get(), first[i], counts[i], static_cast<int64_t*>(S.cells.p),
+                     static_cast<int64_t*>(S.totals.p), S.det.p, static_cast<uint64_t*>(S.detn.p), S.st,
+                     VMC_RUN_ZERO, false, nullptr);
+        ck(cudaEventRecord(e1, S.st), "event");
+        ck(cudaStreamSynchronize(S.st), "run");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        S.ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ck(cudaMemcpy(&S.ndet, S.detn.p, sizeof(uint64_t), cudaMemcpyDeviceToHost), "det count");
+        check_launch_errors(S.plan.get());
+      });
+      if (S.code) S.err = g_last_error;
+    };
+    std::vector<std::thread> pool;
+    for (int i = 0; i < ndev; ++i) pool.emplace_back(worker, i);
+    for (auto& th : pool) th.join();
+    auto cleanup = [&] {
+      for (auto& S : slot)
+        if (S.st) {
+          cudaSetDevice(S.plan ? S.plan->device : 0);
+          cudaStreamDestroy(S.st);
+          S.st = nullptr;
+        }
+    };
+    for (int i = 0; i < ndev; ++i)
+      if (slot[i].code) {
+        cleanup();
+        throw VmcError(slot[i].code, slot[i].err);
+      }
+    const uint64_t ncells = slot[0].plan->ncells;
+    double red_ms = 0.0;
+    try {
+      if (ndev > 1) {
+        // one exchange step: NCCL reduce of the int64 maps + totals onto devices[0]
+        Nccl& N = nccl();
+        std::vector<void*> comms(ndev, nullptr);
+        nck(N.CommInitAll(comms.data(), ndev, devices), "ncclCommInitAll");
+        cudaSetDevice(devices[0]);
+        cudaEvent_t r0, r1;
+        ck(cudaEventCreate(&r0), "event");
+        ck(cudaEventCreate(&r1), "event");
+        ck(cudaEventRecord(r0, slot[0].st), "event");
+        nck(N.GroupStart(), "ncclGroupStart");
+        for (int i = 0; i < ndev; ++i) {
+          cudaSetDevice(devices[i]);
+          nck(N.Reduce(slot[i].cells.p, slot[i].cells.p, ncells, kNcclInt64, kNcclSum, 0, comms[i], slot[i].st),
+              "ncclReduce");
+          nck(N.Reduce(slot[i].totals.p, slot[i].totals.p, 4, kNcclInt64, kNcclSum, 0, comms[i], slot[i].st),
+              "ncclReduce");
+        }
+        nck(N.GroupEnd(), "ncclGroupEnd");
+        cudaSetDevice(devices[0]);
+        ck(cudaEventRecord(r1, slot[0].st), "event");
+        for (int i = 0; i < ndev; ++i) {
+          cudaSetDevice(devices[i]);
+          ck(cudaStreamSynchronize(slot[i].st), "reduce");
+        }
+        float ms = 0.f;
+        cudaSetDevice(devices[0]);
+        cudaEventElapsedTime(&ms, r0, r1);
+        red_ms = ms;
+        cudaEventDestroy(r0);
+        cudaEventDestroy(r1);
+        for (int i = 0; i < ndev; ++i)
+          if (N.CommDestroy) N.CommDestroy(comms[i]);
+      }
+      cudaSetDevice(devices[0]);
+      if (cells_out)
+        ck(cudaMemcpy(cells_out, slot[0].cells.p, ncells * sizeof(int64_t), cudaMemcpyDeviceToHost), "download");
+      int64_t tot[4];
+      ck(cudaMemcpy(tot, slot[0].totals.p, sizeof tot, cudaMemcpyDeviceToHost), "download");
+      if (totals_out) {
+        totals_out->deposited_q = tot[0];
+        totals_out->escaped_q = tot[1];
+        totals_out->killed_q = tot[2];
+        totals_out->truncated_q = tot[3];
+        totals_out->quantum = vmc_quantum_for(config->photon_count);
+      }
+      // detector records: gather in device order, then sort by photon index
+      uint64_t total_det = 0, stored = 0;
+      for (int i = 0; i < ndev; ++i) {
+        total_det += slot[i].ndet;
+        const uint64_t keep = std::min(slot[i].ndet, cap);
+        if (det_out && keep) {
+          const uint64_t room = cap > stored ? cap - stored : 0;
+          const uint64_t take = std::min(keep, room);
+          if (take) {
+            cudaSetDevice(devices[i]);
+            ck(cudaMemcpy(static_cast<unsigned char*>(det_out) + stored * stride, slot[i].det.p, take * stride,
+                          cudaMemcpyDeviceToHost),
+               "download det");
+            stored += take;
+          }
+        }
+      }
+      if (det_out) sort_records(static_cast<unsigned char*>(det_out), stored, stride);
+      if (det_count_out) *det_count_out = config->ndet > 0 ? total_det : 0;
+      for (int i = 0; i < ndev; ++i)
+        if (per_device_ms) per_device_ms[i] = slot[i].ms;
+      if (reduce_ms) *reduce_ms = red_ms;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int vmc_partition(int strategy, uint64_t total, int ndev, const vmc_device_profile* devices, uint64_t* counts_out) {
+  return guarded([&] {
+    if (ndev < 1 || !devices) fail_validation("partition: no devices");
+    std::vector<vmc::DeviceModel> dev(ndev);
+    for (int i = 0; i < ndev; ++i) dev[i] = {devices[i].cores, devices[i].a, devices[i].t0};
+    const std::vector<uint64_t> n = vmc::partition_photons(strategy, total, dev);
+    std::copy(n.begin(), n.end(), counts_out);
+  });
+}
+
+double vmc_model_makespan(int ndev, const uint64_t* counts, const vmc_device_profile* devices) {
+  std::vector<vmc::DeviceModel> dev(ndev);
+  for (int i = 0; i < ndev; ++i) dev[i] = {devices[i].cores, devices[i].a, devices[i].t0};
+  return vmc::model_makespan(std::vector<uint64_t>(counts, counts + ndev), dev);
+}
+
+int vmc_plan_create(const vmc_scene* scene, const vmc_config* config, int device, vmc_plan** out) {
+  return guarded([&] {
+    if (!out) fail_validation("null plan output");
+    std::unique_ptr<vmc_plan> P(new vmc_plan);
+    plan_init(P.get(), scene, config, device);
+    *out = P.release();
+  });
+}
+
+int vmc_plan_destroy(vmc_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    cudaSetDevice(plan->device);
+    delete plan;
+  });
+}
+
+uint64_t vmc_plan_cell_count(const vmc_plan* plan) { return plan ? plan->ncells : 0; }
+
+int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, int64_t* d_cells, int64_t* d_totals,
+                 void* d_det, uint64_t* d_det_count, void* stream, uint32_t flags) {
+  return guarded([&] {
+    if (!plan) fail_validation("null plan");
+    plan_enqueue(plan, first_index, count, d_cells, d_totals, d_det, d_det_count, static_cast<cudaStream_t>(stream),
+                 flags, false, nullptr);
+  });
+}
+
+int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_photon_trace* out) {
+  return guarded([&] {
+    if (!plan) fail_validation("null plan");
+    ck(cudaSetDevice(plan->device), "cudaSetDevice");
+    DevBuf cells, totals, det, detn, tr;
+    cells.alloc(plan->ncells * sizeof(int64_t), plan->device);
+    totals.alloc(4 * sizeof(int64_t), plan->device);
+    const uint64_t cap = plan->cfg.ndet > 0 ? plan->cfg.det_capacity : 0;
+    det.alloc(cap * plan->rec_stride, plan->device);
+    detn.alloc(sizeof(uint64_t), plan->device);
+    tr.alloc(count * sizeof(vmc_photon_trace), plan->device);
+    plan_enqueue(plan, first_index, count, static_cast<int64_t*>(cells.p), static_cast<int64_t*>(totals.p), det.p,
+                 static_cast<uint64_t*>(detn.p), nullptr, VMC_RUN_ZERO, true, static_cast<vmc_photon_trace*>(tr.p));
+    ck(cudaDeviceSynchronize(), "trace run");
+    if (count) ck(cudaMemcpy(out, tr.p, count * sizeof(vmc_photon_trace), cudaMemcpyDeviceToHost), "download trace");
+    check_launch_errors(plan);
+  });
+}
+
+int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags) {
+  (void)flags;
+  return plan ? 1 : 0;
+}
+
+}  // extern "C"

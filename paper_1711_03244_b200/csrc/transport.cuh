@@ -1,0 +1,730 @@
+// transport.cuh — K1, the persistent photon-transport kernel (sm_100a).
+//
+// One CUDA thread = one photon stream at a time. Persistent CTAs (grid = SMs x
+// resident CTAs); when a lane's photon terminates, the warp claims the next
+// global photon indices with ONE atomicAdd on a device counter and relaunches
+// in place (the GPU form of GroupCounter::claim + the run_group worker loop,
+// proj/core/include/voxmc/scheduler.hpp:64-86, proj/core/src/scheduler.cpp:286-305).
+//
+// The walk restates run_photon (proj/core/src/transport.cpp:310-358) with
+// advance (:161-225), boundary_distance (:49-73), hg_scatter (:120-147),
+// handle_interface (:227-298) and roulette (:300-306), consuming the RNG in
+// exactly the reference's order, so photon k draws the
+// same u64 stream as the reference photon k.
+//
+// Two arithmetic instantiations:
+//   float  — the product path. Deposits are coalesced per (voxel, gate) run:
+//            the run's absorbed weight is w_run_start - w (exact by Sterbenz
+//            for the usual case), quantized once, and added with one integer
+//            atomic. Per-photon dispositions are kept in the same fixed-point
+//            quanta, so the energy identity closes in integers.
+//   double — parity mode: per-step llround deposits and double dispositions,
+//            operation-for-operation the reference (compiled with --fmad=false
+//            so it matches the reference built without FMA contraction up to
+//            libm-vs-CUDA log/exp rounding).
+//
+// Fluence cells are int64 fixed point in the reference quantum
+// (proj/core/src/fluence.cpp:11-14); the device adds them with
+// red.global.add.u64, or into a per-CTA shared-memory "hot box" around the
+// source (native 32-bit shared atomics, lo/hi split with exact carry) that is
+// flushed once at kernel exit.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+#include "../../include/vmc.h"
+#include "rng.cuh"
+
+namespace vmc {
+
+constexpr int kBlock = 256;  // threads per CTA of K1
+constexpr int kMaxDet = 16;
+constexpr int kMaxDetMedia = 8;
+constexpr double kLightMmPerNs = 299.792458;  // types.hpp:16
+
+// Per-label optical data, staged in shared memory at CTA start.
+template <typename Real>
+struct alignas(16) Medium {
+  Real mua, mus, inv_mus, ns_per_mm;  // ns_per_mm = n / c
+  Real mm_per_ns, n, g, hg_a;         // hg_a = (1+g^2)/(2g)
+  Real hg_b, hg_c, hg_d, hg_e;        // hg_b = 1/(2g), hg_c = 1-g^2, hg_d = 1-g, hg_e = 2g
+  int nclass;                          // media with equal (double) n share a class
+  int iso;                             // |g| < 1e-6
+  int pad0, pad1;
+};
+
+struct KernelArgs {
+  const uint8_t* labels;
+  int nx, ny, nz, pad0;
+  long long nxy, nvox;
+  double h;
+  int nmedia, iso_source;
+  const void* media;  // Medium<Real>[nmedia]
+  double src_pos[3];
+  double dir0[3];      // normalized pencil direction
+  double pos0[3];      // nudged pencil launch point
+  int v0[3];           // pencil launch voxel
+  int lab0;
+  uint64_t seed, first, count;
+  unsigned long long* claim;  // photon-claim counter (zeroed before launch)
+  double tmax, rthr, inv_rmult;
+  int rmult, reflect;
+  int ngates, pad1;
+  double inv_gate_w;
+  double qscale;  // 1 / quantum
+  long long* cells;
+  long long* totals;  // [4] deposited, escaped, killed, truncated quanta
+  // shared-memory hot box (cells of all gates), disabled when box_cells == 0
+  int bx0, by0, bz0, bnx, bny, bnz, box_cells, pad2;
+  // detectors
+  int ndet, nppath, rec_stride, pad3;
+  double det[kMaxDet][4];
+  unsigned char* det_out;
+  unsigned long long* det_count;
+  unsigned long long det_cap;
+  vmc_photon_trace* trace;
+  int* error_flag;  // set to 1 when a launch point falls outside the grid
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+
+template <typename Real>
+struct RealTraits;
+template <>
+struct RealTraits<float> {
+  static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
+  static __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+};
+template <>
+struct RealTraits<double> {
+  static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+  static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+};
+
+// pick component `axis` of (x, y, z) without dynamic register indexing
+template <typename T>
+__device__ __forceinline__ T sel3(int axis, T x, T y, T z) {
+  return axis == 0 ? x : (axis == 1 ? y : z);
+}
+
+// 64-bit add into a shared-memory cell stored as two 32-bit words, with native
+// 32-bit shared atomics; the carry out of the low word is propagated exactly
+// once by the thread whose add wrapped it.
+__device__ __forceinline__ void smem_add_u64(unsigned int* lo, unsigned int* hi, unsigned long long v) {
+  const unsigned int vlo = static_cast<unsigned int>(v);
+  unsigned int vhi = static_cast<unsigned int>(v >> 32);
+  const unsigned int old = atomicAdd(lo, vlo);
+  vhi += (old + vlo < old) ? 1u : 0u;
+  if (vhi) atomicAdd(hi, vhi);
+}
+
+template <typename Real, bool kGates, bool kDet, bool kTrace>
+struct Walk;
+
+// ---------------------------------------------------------------------------
+// The kernel body (shared by both precisions).
+
+template <typename Real, bool kGates, bool kDet, bool kTrace>
+__device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned char* smem) {
+  using Tr = RealTraits<Real>;
+  constexpr bool kF32 = std::is_same<Real, float>::value;
+  using Rng = Xs128p<kTrace>;
+
+  // ---- shared memory: media table, per-CTA hot box (lo/hi words) ---------
+  Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem);
+  unsigned int* box_lo = reinterpret_cast<unsigned int*>(smem + sizeof(Medium<Real>) * A.nmedia);
+  unsigned int* box_hi = box_lo + A.box_cells;
+  {
+    const Medium<Real>* gm = static_cast<const Medium<Real>*>(A.media);
+    const int nwords = static_cast<int>(sizeof(Medium<Real>) / 4) * A.nmedia;
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x)
+      reinterpret_cast<int*>(sm_media)[i] = reinterpret_cast<const int*>(gm)[i];
+    for (int i = threadIdx.x; i < 2 * A.box_cells; i += blockDim.x) box_lo[i] = 0u;
+  }
+  __syncthreads();
+
+  const int nx = A.nx, ny = A.ny, nz = A.nz;
+  const long long nxy = A.nxy;
+  const Real h = static_cast<Real>(A.h);
+  const Real tmax = static_cast<Real>(A.tmax);
+  const Real rthr = static_cast<Real>(A.rthr);
+  const Real rmult = static_cast<Real>(A.rmult);
+  const Real inv_rmult = static_cast<Real>(A.inv_rmult);
+  const Real inv_gate_w = static_cast<Real>(A.inv_gate_w);
+  const float qscale_f = static_cast<float>(A.qscale);
+  const int lane = threadIdx.x & 31;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+
+  // per-thread fixed-point disposition totals
+  long long acc_dep = 0, acc_esc = 0, acc_kill = 0, acc_trunc = 0;
+
+  // photon state
+  bool alive = false;
+  bool exhausted = false;  // warp-uniform: counter ran past `count`
+  uint64_t idx = 0;
+  Rng rng;
+  rng.a = rng.b = 0;
+  Real px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, ix = 0, iy = 0, iz = 0;
+  Real w = 0, t = 0, rs = 0;
+  int vx = 0, vy = 0, vz = 0, lab = 0;
+  long long cell = 0;
+  int gate = 0;
+  Real run_w0 = 0;          // float path: weight at the start of the current run
+  double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // per-photon (double path / trace)
+  uint32_t steps = 0, nscat = 0;
+  bool detected = false;
+  Real ppath[kDet ? kMaxDetMedia : 1];
+#pragma unroll
+  for (int m = 0; m < (kDet ? kMaxDetMedia : 1); ++m) ppath[m] = 0;
+
+  auto deposit = [&](long long c, int gt, int bvx, int bvy, int bvz, long long q) {
+    if (q == 0) return;
+    if (A.box_cells) {
+      const unsigned ux = static_cast<unsigned>(bvx - A.bx0), uy = static_cast<unsigned>(bvy - A.by0),
+                     uz = static_cast<unsigned>(bvz - A.bz0);
+      if (ux < static_cast<unsigned>(A.bnx) && uy < static_cast<unsigned>(A.bny) &&
+          uz < static_cast<unsigned>(A.bnz)) {
+        const int bi = static_cast<int>(ux + A.bnx * (uy + A.bny * (uz + A.bnz * gt)));
+        smem_add_u64(box_lo + bi, box_hi + bi, static_cast<unsigned long long>(q));
+        return;
+      }
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (c + A.nvox * gt),
+              static_cast<unsigned long long>(q));
+  };
+  auto quant = [&](Real x) -> long long {
+    if constexpr (kF32) {
+      return __float2ll_rn(x * qscale_f);
+    } else {
+      return llround(x * A.qscale);
+    }
+  };
+  auto gate_of = [&](Real tt) -> int {
+    if constexpr (kGates) {
+      int g = static_cast<int>(tt * inv_gate_w);  // tt >= 0: truncation == floor
+      return g < A.ngates - 1 ? g : A.ngates - 1;
+    } else {
+      return 0;
+    }
+  };
+  auto set_dir = [&](Real ax_, Real ay_, Real az_) {  // transport.cpp:77-81
+    dx = ax_;
+    dy = ay_;
+    dz = az_;
+    ix = ax_ != Real(0) ? Tr::rcp(ax_) : Tr::inf();
+    iy = ay_ != Real(0) ? Tr::rcp(ay_) : Tr::inf();
+    iz = az_ != Real(0) ? Tr::rcp(az_) : Tr::inf();
+  };
+  auto scat_len = [&]() -> Real {  // transport.cpp:14-17
+    const Real u = rng.template unit<Real>();
+    if constexpr (kF32) {
+      // u == 0 (p = 2^-24) stands for the reference's [0, 2^-24) cell: use 2^-25.
+      return -logf(u > 0.0f ? u : 0x1p-25f);
+    } else {
+      return -log(u > 0.0 ? u : 4.9406564584124654e-324);
+    }
+  };
+  auto finish = [&](int kind) {  // 0 escaped 1 killed 2 truncated
+    if constexpr (kTrace) {
+      vmc_photon_trace tr;
+      tr.draws = rng.draws;
+      tr.steps = steps;
+      tr.scatters = nscat;
+      tr.flags = (kind == 0 ? 1u : (kind == 1 ? 2u : 4u)) | (detected ? 8u : 0u);
+      detected = false;
+      tr.deposited = pd_dep;
+      tr.escaped = pd_esc;
+      tr.killed = pd_kill;
+      tr.truncated = pd_trunc;
+      A.trace[idx - A.first] = tr;
+    }
+    if constexpr (!kF32) {
+      acc_dep += llround(pd_dep * A.qscale);
+      acc_esc += llround(pd_esc * A.qscale);
+      acc_kill += llround(pd_kill * A.qscale);
+      acc_trunc += llround(pd_trunc * A.qscale);
+    }
+    alive = false;
+  };
+
+  for (;;) {
+    // ---- refill dead lanes: one atomicAdd per warp (dynamic claiming) ----
+    if (!exhausted) {
+      const unsigned need = __ballot_sync(0xffffffffu, !alive);
+      if (need) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.claim, static_cast<unsigned long long>(__popc(need)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + __popc(need) >= A.count) exhausted = true;
+        if (!alive) {
+          const unsigned long long my = base + __popc(need & lanemask_lt);
+          if (my < A.count) {
+            // ---- launch, transport.cpp:83-106 ----
+            idx = A.first + my;
+            rng.seed(A.seed, idx);
+            Real ux, uy, uz;
+            if (A.iso_source) {
+              const Real ct = Real(2) * rng.template unit<Real>() - Real(1);
+              const Real u2 = rng.template unit<Real>();
+              Real st, cphi, sphi;
+              if constexpr (kF32) {
+                st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+                sincospif(2.0f * u2, &sphi, &cphi);
+              } else {
+                st = sqrt(fmax(0.0, 1.0 - ct * ct));
+                const double phi = 2.0 * 3.14159265358979323846 * u2;
+                sincos(phi, &sphi, &cphi);
+              }
+              ux = st * cphi;
+              uy = st * sphi;
+              uz = ct;
+              // nudge + voxel_of in double (the 1e-6 mm nudge is below FP32 ulp)
+              const double qx = A.src_pos[0] + static_cast<double>(ux) * 1e-6;
+              const double qy = A.src_pos[1] + static_cast<double>(uy) * 1e-6;
+              const double qz = A.src_pos[2] + static_cast<double>(uz) * 1e-6;
+              vx = static_cast<int>(floor(qx / A.h));
+              vy = static_cast<int>(floor(qy / A.h));
+              vz = static_cast<int>(floor(qz / A.h));
+              px = static_cast<Real>(qx);
+              py = static_cast<Real>(qy);
+              pz = static_cast<Real>(qz);
+              if (vx < 0 || vy < 0 || vz < 0 || vx >= nx || vy >= ny || vz >= nz) {
+                atomicExch(A.error_flag, 1);
+                vx = vy = vz = 0;
+                ux = uy = 0;
+                uz = 1;
+              }
+              lab = __ldg(A.labels + (vx + nx * (vy + static_cast<long long>(ny) * vz)));
+            } else {
+              ux = static_cast<Real>(A.dir0[0]);
+              uy = static_cast<Real>(A.dir0[1]);
+              uz = static_cast<Real>(A.dir0[2]);
+              px = static_cast<Real>(A.pos0[0]);
+              py = static_cast<Real>(A.pos0[1]);
+              pz = static_cast<Real>(A.pos0[2]);
+              vx = A.v0[0];
+              vy = A.v0[1];
+              vz = A.v0[2];
+              lab = A.lab0;
+            }
+            set_dir(ux, uy, uz);
+            cell = vx + nx * (vy + static_cast<long long>(ny) * vz);
+            w = Real(1);
+            t = Real(0);
+            rs = scat_len();
+            gate = 0;
+            run_w0 = Real(1);
+            steps = nscat = 0;
+            pd_dep = pd_esc = pd_kill = pd_trunc = 0;
+            if constexpr (kDet) {
+#pragma unroll
+              for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] = 0;
+            }
+            alive = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, alive)) break;
+    if (!alive) continue;
+
+    // ---- one advance() step, transport.cpp:161-225 ----
+    const Medium<Real>& M = sm_media[lab];
+    if constexpr (kTrace) ++steps;
+    // boundary_distance, transport.cpp:49-73
+    Real tb0, tb1, tb2;
+    {
+      const Real plx = static_cast<Real>(vx + (dx > Real(0) ? 1 : 0)) * h;
+      const Real ply = static_cast<Real>(vy + (dy > Real(0) ? 1 : 0)) * h;
+      const Real plz = static_cast<Real>(vz + (dz > Real(0) ? 1 : 0)) * h;
+      const Real t0_ = (plx - px) * ix, t1_ = (ply - py) * iy, t2_ = (plz - pz) * iz;
+      tb0 = dx != Real(0) ? (t0_ > Real(0) ? t0_ : Real(0)) : Tr::inf();
+      tb1 = dy != Real(0) ? (t1_ > Real(0) ? t1_ : Real(0)) : Tr::inf();
+      tb2 = dz != Real(0) ? (t2_ > Real(0) ? t2_ : Real(0)) : Tr::inf();
+    }
+    int axis = 0;
+    Real d_b = tb0;
+    if (tb1 < d_b) {
+      d_b = tb1;
+      axis = 1;
+    }
+    if (tb2 < d_b) {
+      d_b = tb2;
+      axis = 2;
+    }
+    Real d_s;
+    if constexpr (kF32) {
+      d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();
+    } else {
+      d_s = M.mus > 0.0 ? rs / M.mus : Tr::inf();
+    }
+    const Real ns = M.ns_per_mm;
+    const Real remaining = tmax - t;
+    Real d = d_b < d_s ? d_b : d_s;  // std::min(d_boundary, d_scatter)
+    const bool horizon = d * ns >= remaining;
+    if (horizon) {
+      if constexpr (kF32) {
+        d = fmaxf(0.0f, remaining * M.mm_per_ns);
+      } else {
+        d = fmax(0.0, remaining / ns);
+      }
+    }
+    // Beer-Lambert, exp_neg transport.cpp:22-27
+    Real w1;
+    {
+      const Real x = M.mua * d;
+      Real e;
+      if (x < Real(0.01)) {
+        e = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
+      } else {
+        if constexpr (kF32) {
+          e = __expf(-x);
+        } else {
+          e = exp(-x);
+        }
+      }
+      w1 = w * e;
+    }
+    const Real t_start = t;
+    if constexpr (!kF32) {
+      // per-step deposit into the pre-step voxel (transport.cpp:323-327)
+      const Real dw = w - w1;
+      if (dw != 0.0) {
+        deposit(cell, gate_of(t_start), vx, vy, vz, llround(dw * A.qscale));
+        pd_dep += dw;
+      }
+    } else if constexpr (kTrace) {
+      pd_dep += static_cast<double>(w - w1);
+    }
+    w = w1;
+    t += d * ns;
+    if constexpr (kDet) {
+#pragma unroll
+      for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] += (lab == m + 1) ? d : Real(0);
+    }
+
+    if (horizon) {  // StepKind::Terminated
+      t = tmax;
+      if constexpr (kF32) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, vx, vy, vz, q);
+        acc_dep += q;
+        acc_trunc += quant(w);
+      }
+      pd_trunc += w;
+      finish(2);
+      continue;
+    }
+
+    if (d_s <= d_b) {
+      // ---- scatter: move, hg_scatter (transport.cpp:126-147), new length ----
+      px += dx * d;
+      py += dy * d;
+      pz += dz * d;
+      if constexpr (kTrace || kDet) ++nscat;
+      Real ct;
+      {
+        const Real xi = rng.template unit<Real>();
+        if (M.iso) {
+          ct = Real(2) * xi - Real(1);
+        } else {
+          if constexpr (kF32) {
+            const float f = M.hg_c / (M.hg_d + M.hg_e * xi);
+            ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
+          } else {
+            const double g = M.g;
+            const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
+            ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
+            ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
+          }
+        }
+      }
+      Real st;
+      if constexpr (kF32) {
+        st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+      } else {
+        st = sqrt(fmax(0.0, 1.0 - ct * ct));
+      }
+      Real cp, sp;
+      for (;;) {  // sample_azimuth, transport.cpp:32-44
+        const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
+        const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
+        const Real r2 = ax_ * ax_ + ay_ * ay_;
+        if (r2 > Real(1e-12) && r2 <= Real(1)) {
+          Real k;
+          if constexpr (kF32) {
+            k = rsqrtf(r2);
+          } else {
+            k = 1.0 / sqrt(r2);
+          }
+          cp = ax_ * k;
+          sp = ay_ * k;
+          break;
+        }
+      }
+      Real ox, oy, oz;
+      if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
+        ox = st * cp;
+        oy = st * sp;
+        oz = dz > Real(0) ? ct : -ct;
+      } else {
+        if constexpr (kF32) {
+          const float one_m = 1.0f - dz * dz;
+          const float rden = rsqrtf(one_m);
+          const float den = one_m * rden;
+          const float sr = st * rden;
+          ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
+          oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
+          oz = -st * cp * den + dz * ct;
+        } else {
+          const double den = sqrt(1.0 - dz * dz);
+          ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
+          oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
+          oz = -st * cp * den + dz * ct;
+        }
+      }
+      {
+        const Real n2 = ox * ox + oy * oy + oz * oz;
+        if constexpr (kF32) {
+          if (fabsf(n2 - 1.0f) > 1e-6f) {
+            const float k = rsqrtf(n2);
+            ox *= k;
+            oy *= k;
+            oz *= k;
+          }
+        } else {
+          if (fabs(n2 - 1.0) > 1e-12) {
+            const double k = 1.0 / sqrt(n2);
+            ox *= k;
+            oy *= k;
+            oz *= k;
+          }
+        }
+      }
+      set_dir(ox, oy, oz);
+      rs = scat_len();
+      // roulette after a scatter only (transport.cpp:333-343, 300-306)
+      if (w < rthr) {
+        const Real before = w;
+        const bool survive = rng.template unit<Real>() < inv_rmult;
+        if constexpr (kF32) {
+          const long long q = quant(run_w0 - w);
+          deposit(cell, gate, vx, vy, vz, q);
+          acc_dep += q;
+        }
+        if (!survive) {
+          if constexpr (kF32) acc_kill += quant(before);
+          pd_kill += before;
+          finish(1);
+          continue;
+        }
+        w *= rmult;
+        if constexpr (kF32) {
+          acc_kill += quant(before) - quant(w);
+          run_w0 = w;
+        }
+        pd_kill += before - w;
+      }
+      if constexpr (kGates && kF32) {
+        const int ng = gate_of(t);
+        if (ng != gate) {
+          const long long q = quant(run_w0 - w);
+          deposit(cell, gate, vx, vy, vz, q);
+          acc_dep += q;
+          run_w0 = w;
+          gate = ng;
+        }
+      }
+      continue;
+    }
+
+    // ---- land exactly on the face (transport.cpp:197-211) ----
+    if constexpr (kF32) {
+      rs = fmaxf(0.0f, rs - d * M.mus);
+    } else {
+      rs = fmax(0.0, rs - d * M.mus);
+    }
+    px += dx * d;
+    py += dy * d;
+    pz += dz * d;
+    const Real dax = sel3(axis, dx, dy, dz);
+    const int stp = dax > Real(0) ? 1 : -1;
+    int nvx = vx, nvy = vy, nvz = vz;
+    long long ncell = cell;
+    if (axis == 0) {
+      px = static_cast<Real>(vx + (stp > 0 ? 1 : 0)) * h;
+      nvx += stp;
+      ncell += stp;
+    } else if (axis == 1) {
+      py = static_cast<Real>(vy + (stp > 0 ? 1 : 0)) * h;
+      nvy += stp;
+      ncell += stp * static_cast<long long>(nx);
+    } else {
+      pz = static_cast<Real>(vz + (stp > 0 ? 1 : 0)) * h;
+      nvz += stp;
+      ncell += stp * nxy;
+    }
+    const bool exterior = nvx < 0 || nvy < 0 || nvz < 0 || nvx >= nx || nvy >= ny || nvz >= nz;
+    const int nlab = exterior ? 0 : static_cast<int>(__ldg(A.labels + ncell));
+    const int c1 = M.nclass, c2 = sm_media[nlab].nclass;
+    bool move = false, exited = false;
+    if (!exterior && c1 == c2) {
+      move = true;  // same refractive index: inline update (transport.cpp:218-223)
+    } else if (exterior && !A.reflect) {
+      exited = true;  // TerminateAtBoundary (transport.cpp:234-237)
+    } else if (c1 == c2) {
+      exited = exterior;  // identity interface, n1 == n2 (transport.cpp:242-252)
+      move = !exterior;
+    } else {
+      // Fresnel / TIR, handle_interface transport.cpp:254-297
+      const Real n1 = M.n, n2 = sm_media[nlab].n;
+      const Real ci = dax < Real(0) ? -dax : dax;
+      Real si2 = Real(1) - ci * ci;
+      si2 = si2 > Real(0) ? si2 : Real(0);
+      const Real eta = n1 / n2;
+      const Real st2 = eta * eta * si2;
+      if (st2 > Real(1)) {  // total internal reflection: deterministic flip
+        set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
+      } else {
+        Real cost;
+        if constexpr (kF32) {
+          cost = sqrtf(1.0f - st2);
+        } else {
+          cost = sqrt(1.0 - st2);
+        }
+        const Real rsp = (n1 * ci - n2 * cost) / (n1 * ci + n2 * cost);
+        const Real rpp = (n1 * cost - n2 * ci) / (n1 * cost + n2 * ci);
+        const Real R = Real(0.5) * (rsp * rsp + rpp * rpp);
+        if (rng.template unit<Real>() < R) {
+          set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
+        } else {
+          Real qx = axis == 0 ? (dax > Real(0) ? cost : -cost) : dx * eta;
+          Real qy = axis == 1 ? (dax > Real(0) ? cost : -cost) : dy * eta;
+          Real qz = axis == 2 ? (dax > Real(0) ? cost : -cost) : dz * eta;
+          Real k;
+          if constexpr (kF32) {
+            k = rsqrtf(qx * qx + qy * qy + qz * qz);
+          } else {
+            k = 1.0 / sqrt(qx * qx + qy * qy + qz * qz);
+          }
+          set_dir(qx * k, qy * k, qz * k);
+          exited = exterior;
+          move = !exterior;
+        }
+      }
+    }
+
+    if (exited) {  // ExitedDomain: escaped += w (transport.cpp:348-350)
+      if constexpr (kF32) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, vx, vy, vz, q);
+        acc_dep += q;
+        acc_esc += quant(w);
+      }
+      pd_esc += w;
+      if constexpr (kDet) {
+        int hit = -1;
+        for (int k = 0; k < A.ndet; ++k) {
+          const double ex = static_cast<double>(px) - A.det[k][0];
+          const double ey = static_cast<double>(py) - A.det[k][1];
+          const double ez = static_cast<double>(pz) - A.det[k][2];
+          if (ex * ex + ey * ey + ez * ez <= A.det[k][3] * A.det[k][3]) {
+            hit = k;
+            break;
+          }
+        }
+        const unsigned am = __activemask();
+        const unsigned hm = __ballot_sync(am, hit >= 0);
+        if constexpr (kTrace) detected = hit >= 0;
+        if (hm) {
+          const int leader = __ffs(hm) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(A.det_count, static_cast<unsigned long long>(__popc(hm)));
+          base = __shfl_sync(am, base, leader);
+          if (hit >= 0) {
+            const unsigned long long slot = base + __popc(hm & lanemask_lt);
+            if (slot < A.det_cap) {
+              unsigned char* rec = A.det_out + slot * static_cast<unsigned long long>(A.rec_stride);
+              vmc_det_record_head hd;
+              hd.photon_index = idx;
+              hd.det_id = static_cast<uint32_t>(hit);
+              hd.nscat = nscat;
+              hd.w_exit = static_cast<float>(w);
+              hd.t_exit_ns = static_cast<float>(t);
+              *reinterpret_cast<vmc_det_record_head*>(rec) = hd;
+              float* pp = reinterpret_cast<float*>(rec + sizeof(vmc_det_record_head));
+#pragma unroll
+              for (int m = 0; m < kMaxDetMedia; ++m)
+                if (m < A.nppath) pp[m] = static_cast<float>(ppath[m]);
+            }
+          }
+        }
+      }
+      finish(0);
+      continue;
+    }
+    if (move) {
+      if constexpr (kF32) {
+        const int ng = gate_of(t);
+        // a new voxel (or gate) closes the current deposit run
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, vx, vy, vz, q);
+        acc_dep += q;
+        run_w0 = w;
+        gate = ng;
+      }
+      vx = nvx;
+      vy = nvy;
+      vz = nvz;
+      cell = ncell;
+      lab = nlab;
+    } else if constexpr (kGates && kF32) {
+      const int ng = gate_of(t);
+      if (ng != gate) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, vx, vy, vz, q);
+        acc_dep += q;
+        run_w0 = w;
+        gate = ng;
+      }
+    }
+  }
+
+  // ---- epilogue: dispositions (warp reduce), hot-box flush -------------
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc_dep += __shfl_xor_sync(0xffffffffu, acc_dep, o);
+    acc_esc += __shfl_xor_sync(0xffffffffu, acc_esc, o);
+    acc_kill += __shfl_xor_sync(0xffffffffu, acc_kill, o);
+    acc_trunc += __shfl_xor_sync(0xffffffffu, acc_trunc, o);
+  }
+  if (lane == 0) {
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(A.totals);
+    if (acc_dep) atomicAdd(tot + 0, static_cast<unsigned long long>(acc_dep));
+    if (acc_esc) atomicAdd(tot + 1, static_cast<unsigned long long>(acc_esc));
+    if (acc_kill) atomicAdd(tot + 2, static_cast<unsigned long long>(acc_kill));
+    if (acc_trunc) atomicAdd(tot + 3, static_cast<unsigned long long>(acc_trunc));
+  }
+  if (A.box_cells) {
+    __syncthreads();
+    const int per_gate = A.bnx * A.bny * A.bnz;
+    for (int i = threadIdx.x; i < A.box_cells; i += blockDim.x) {
+      const unsigned long long v =
+          (static_cast<unsigned long long>(box_hi[i]) << 32) | static_cast<unsigned long long>(box_lo[i]);
+      if (v) {
+        const int gt = i / per_gate;
+        int r = i - gt * per_gate;
+        const int bx = r % A.bnx;
+        r /= A.bnx;
+        const int by = r % A.bny;
+        const int bz = r / A.bny;
+        const long long c = (A.bx0 + bx) + nx * ((A.by0 + by) + static_cast<long long>(ny) * (A.bz0 + bz));
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (c + A.nvox * gt), v);
+      }
+    }
+  }
+}
+
+}  // namespace vmc

@@ -1,0 +1,39 @@
+// transport_kernels.cu — instantiates K1 for one arithmetic type.
+// Compiled twice by the build: once with -DVMC_REAL=float (FMA contraction on,
+// the product path) and once with -DVMC_REAL=double --fmad=false (parity mode;
+// no contraction, like the reference built with -ffp-contract=off).
+#include "transport.cuh"
+
+#ifndef VMC_REAL
+#define VMC_REAL float
+#endif
+
+namespace vmc {
+
+template <typename Real, bool G, bool D, bool T>
+__global__ void __launch_bounds__(kBlock) k_transport(const __grid_constant__ KernelArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  transport_body<Real, G, D, T>(A, smem);
+}
+
+#define VMC_CAT2(a, b) a##b
+#define VMC_CAT(a, b) VMC_CAT2(a, b)
+
+// Returns the kernel for (gates, detectors, trace); host code launches it with
+// cudaLaunchKernel and sizes the persistent grid by occupancy.
+const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trace) {
+  using R = VMC_REAL;
+  const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
+  switch (key) {
+    case 0: return reinterpret_cast<const void*>(&k_transport<R, false, false, false>);
+    case 1: return reinterpret_cast<const void*>(&k_transport<R, false, false, true>);
+    case 2: return reinterpret_cast<const void*>(&k_transport<R, false, true, false>);
+    case 3: return reinterpret_cast<const void*>(&k_transport<R, false, true, true>);
+    case 4: return reinterpret_cast<const void*>(&k_transport<R, true, false, false>);
+    case 5: return reinterpret_cast<const void*>(&k_transport<R, true, false, true>);
+    case 6: return reinterpret_cast<const void*>(&k_transport<R, true, true, false>);
+    default: return reinterpret_cast<const void*>(&k_transport<R, true, true, true>);
+  }
+}
+
+}  // namespace vmc

@@ -1,0 +1,153 @@
+"""Pins the oracles before anything is checked against them (CPU only).
+
+* oracle/_ref (the compiled reference) reproduces the reference's own recorded
+  checksum (proj/test_output.txt:25) and the Appendix-A vectors committed in
+  tests/golden/golden.json;
+* the plain-C restatement (oracle/voxmc_oracle.c) reproduces the reference
+  built with FMA contraction off BIT FOR BIT, and the default (FMA) reference
+  to rounding;
+* ref_walk (the derived oracle for gates/detectors) equals
+  simulate_photon_trace photon by photon.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1711_03244_b200 as v
+from paper_1711_03244_b200.scene import Benchmark, benchmark_preset
+
+NOFMA = os.path.join(oracle.HERE, "_ref", "libvoxmc_ref_nofma.so")
+
+
+def test_rng_kat_reference(ref, golden):
+    assert golden["mix64_0"] == "e220a8397b1dcdaf"
+    for k in golden["rng"]:
+        out, st, u = ref.rng_kat(k["seed"], k["id"], 16)
+        assert [f"{x:016x}" for x in out] == k["u64"]
+        assert [f"{x:016x}" for x in st] == k["state"]
+        assert u == k["first_unit"]
+    # Appendix A row (20260826, 123456789)
+    row = [k for k in golden["rng"] if k["id"] == 123456789][0]
+    assert row["u64"][:4] == ["8ac56efd89a4bd9b", "b0746c4a7ab67a6f", "a70fc240548d9adb", "de93be79059ca011"]
+    # seed^id aliasing: (0,0) == (1,1)
+    assert golden["rng"][0]["u64"] == golden["rng"][2]["u64"]
+
+
+def test_rng_c_restatement_and_host_stream(corc, golden):
+    from paper_1711_03244_b200.rngs import HostStream
+    for k in golden["rng"]:
+        assert [f"{x:016x}" for x in corc.rng_kat(k["seed"], k["id"], 16)] == k["u64"]
+        hs = HostStream(k["seed"], k["id"])
+        assert [f"{hs.next_u64():016x}" for _ in range(16)] == k["u64"]
+
+
+def test_recorded_checksum_reproduced(ref, golden):
+    """proj/test_output.txt:25 — B1, 1e5 photons, seed 1 -> 428b1d605a48eb37."""
+    st = benchmark_preset(Benchmark.B1)
+    st.config.master_seed = 1
+    st.config.photon_count = 100_000
+    cells, disp, _ = ref.run_group(st.scene, st.config, 0, 100_000, os.cpu_count() or 4)
+    q = ref.quantum_for(100_000)
+    assert oracle.volume_checksum(cells, q) == "428b1d605a48eb37"
+    g = [r for r in golden["runs"] if r["bench"] == "B1"][0]
+    assert int(cells.sum()) == g["raw_sum"] == 622384891573567704
+    assert disp == pytest.approx(g["disp"], rel=1e-12, abs=1e-9)
+
+
+def test_golden_runs_and_photons(ref, golden):
+    for g in golden["runs"]:
+        st = benchmark_preset(Benchmark[g["bench"]])
+        st.config.master_seed = g["seed"]
+        st.config.photon_count = g["photons"]
+        cells, disp, _ = ref.run_group(st.scene, st.config, 0, g["photons"], os.cpu_count() or 4)
+        assert oracle.volume_checksum(cells, g["quantum"]) == g["checksum"]
+    for p in golden["photons"]:
+        st = benchmark_preset(Benchmark[p["bench"]])
+        st.config.master_seed = 1
+        deps, disp = ref.trace(st.scene, st.config, p["index"])
+        assert len(deps) == p["ndeps"]
+        assert disp == p["disp"]
+    # Appendix A: B1 photon 0: 52 deposits, first (30,30,0): 0.0049875158322292279
+    p0 = [p for p in golden["photons"] if p["bench"] == "B1" and p["index"] == 0][0]
+    assert p0["ndeps"] == 52 and p0["first_cell"] == 30 + 60 * 30
+    assert p0["first_dw"] == pytest.approx(0.0049875158322292279, rel=1e-15)
+
+
+@pytest.mark.parametrize("bench", ["B1", "B2"])
+def test_c_restatement_bit_exact_vs_nofma_reference(corc, bench):
+    R0 = oracle.RefLib(NOFMA)
+    st = benchmark_preset(Benchmark[bench])
+    st.config.master_seed = 1
+    st.config.photon_count = 30_000
+    rc, rd, _ = R0.run_group(st.scene, st.config, 0, 30_000, 4)
+    out = corc.walk(st.scene, st.config, 0, 30_000, threads=4)
+    assert np.array_equal(out["cells"], rc)
+    assert out["disp"] == pytest.approx(rd, rel=1e-13, abs=1e-9)
+
+
+def test_c_restatement_vs_fma_reference(ref, corc):
+    st = v.baseline_setup("b2", photons=20_000)
+    a = ref.walk(st.scene, st.config, 0, 20_000, threads=4, traces=True)
+    b = corc.walk(st.scene, st.config, 0, 20_000, threads=4, traces=True)
+    same = (a["traces"]["draws"] == b["traces"]["draws"]).mean()
+    assert same > 0.995
+    assert b["disp"][0] / a["disp"][0] - 1 == pytest.approx(0, abs=1e-3)
+
+
+def test_ref_walk_equals_simulate_photon_trace(ref):
+    st = benchmark_preset(Benchmark.B2)
+    st.config.master_seed = 123
+    w = ref.walk(st.scene, st.config, 0, 300, threads=2, traces=True)["traces"]
+    for i in range(300):
+        _, disp = ref.trace(st.scene, st.config, i)
+        assert [w[i]["deposited"], w[i]["escaped"], w[i]["killed"], w[i]["truncated"]] == disp
+        # per-photon identity (test_transport.cpp:275-291)
+        assert abs(sum(disp) - 1.0) < 1e-9
+
+
+def test_ref_walk_cells_equal_run_group(ref):
+    st = benchmark_preset(Benchmark.B1)
+    st.config.master_seed = 5
+    st.config.photon_count = 5_000
+    w = ref.walk(st.scene, st.config, 0, 5_000, threads=3)
+    rc, _, _ = ref.run_group(st.scene, st.config, 0, 5_000, 2)
+    assert np.array_equal(w["cells"], rc)
+
+
+def test_gate_sum_equals_cw_in_oracles(ref, corc):
+    """Σ over gates == CW map exactly when ngates * Δt == tmax."""
+    st = v.baseline_setup("b1", photons=20_000)
+    cw = ref.walk(st.scene, st.config, 0, 20_000, threads=4)["cells"]
+    st.config.ngates = 10
+    g = ref.walk(st.scene, st.config, 0, 20_000, threads=4)["cells"].reshape(10, -1)
+    assert np.array_equal(g.sum(axis=0), cw)
+    assert (g[1:] > 0).any()  # later gates are populated
+    c = corc.walk(st.scene, st.config, 0, 20_000, threads=4)["cells"].reshape(10, -1)
+    assert (g.sum(axis=1) / c.sum(axis=1) - 1 < 1e-3).all()
+
+
+def test_detector_identities_oracle(ref, corc):
+    st = v.baseline_setup("b3", photons=50_000)
+    a = ref.walk(st.scene, st.config, 0, 50_000, threads=8, cells=False, detectors=True)
+    b = corc.walk(st.scene, st.config, 0, 50_000, threads=8, cells=False, detectors=True)
+    assert a["det_count"] > 50
+    assert abs(a["det_count"] - b["det_count"]) <= max(3, 0.01 * a["det_count"])
+    det = a["det"]
+    media = st.scene.grid.media_array()
+    n = media[1:, 3]
+    mua = media[1:, 0]
+    L = det["ppath_mm"].astype(np.float64)
+    # time of flight = Σ L_m n_m / c
+    assert np.allclose((L * n).sum(axis=1) / 299.792458, det["t_exit_ns"], rtol=1e-5)
+    # no roulette in this scene: exit weight = exp(-Σ mua_m L_m)
+    assert np.allclose(np.exp(-(L * mua).sum(axis=1)), det["w_exit"], rtol=1e-5)
+    assert np.all(np.diff(det["photon_index"].astype(np.int64)) >= 0)
+
+
+def test_reference_quantum(ref):
+    for n in [1, 2, 100, 100_000, 1_000_000, 10**8, 10**9, 2**40]:
+        assert ref.quantum_for(n) == math.ldexp(1.0, -(62 - (n | 1).bit_length()))
+        assert oracle.corc().quantum_for(n) == ref.quantum_for(n)
