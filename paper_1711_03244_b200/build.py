@@ -19,6 +19,7 @@ OBJ_DIR = os.path.join(PKG, "lib", "obj")
 LIB = os.path.join(OUT_DIR, "libvoxmc_b200.so")
 
 NVCC = os.environ.get("NVCC", "nvcc")
+CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
@@ -49,8 +50,11 @@ def _compile(src: str, obj: str, extra, verbose: bool) -> None:
     objp = os.path.join(OBJ_DIR, obj)
     if not _stale(objp, srcp):
         return
-    lang = [] if src.endswith(".cu") else ["-x", "cu"] if False else []
-    cmd = [NVCC] + ARCH + COMMON + extra + lang + ["-c", srcp, "-o", objp]
+    if src.endswith(".cu"):
+        cmd = [NVCC] + ARCH + COMMON + extra + ["-c", srcp, "-o", objp]
+    else:  # host C++ (C++20 for the drop-in API), same visibility rules
+        cmd = [CXX, "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall",
+               "-I", os.path.join(ROOT, "include"), "-I", CSRC] + extra + ["-c", srcp, "-o", objp]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -142,6 +142,7 @@ void validate(const vmc_scene* s, const vmc_config* c) {
     for (int k = 0; k < c->ndet; ++k)
       if (!(c->det[4 * k + 3] > 0.0)) fail_validation("detector radius must be > 0");
   }
+  if (nvox >= (1ull << 31)) fail_validation("volume must have fewer than 2^31 voxels");
   if (static_cast<unsigned long long>(nvox) * static_cast<unsigned>(c->ngates) > (1ull << 40))
     fail_validation("volume x gates too large");
   // launch point (transport.cpp:95-99)

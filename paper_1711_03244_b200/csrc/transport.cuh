@@ -95,12 +95,24 @@ struct RealTraits;
 template <>
 struct RealTraits<float> {
   static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
-  static __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+  // MUFU.RCP (<= 1 ulp): the cached inverse direction only feeds the DDA
+  // plane distances, where one ulp is far below the voxel-landing tolerance.
+  static __device__ __forceinline__ float rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
+  static __device__ __forceinline__ float sqrt_(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
 };
 template <>
 struct RealTraits<double> {
   static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
   static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+  static __device__ __forceinline__ double sqrt_(double x) { return sqrt(x); }
 };
 
 // pick component `axis` of (x, y, z) without dynamic register indexing
@@ -146,7 +158,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   __syncthreads();
 
   const int nx = A.nx, ny = A.ny, nz = A.nz;
-  const long long nxy = A.nxy;
+  const int nxy32 = static_cast<int>(A.nxy);
   const Real h = static_cast<Real>(A.h);
   const Real tmax = static_cast<Real>(A.tmax);
   const Real rthr = static_cast<Real>(A.rthr);
@@ -169,7 +181,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   Real px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, ix = 0, iy = 0, iz = 0;
   Real w = 0, t = 0, rs = 0;
   int vx = 0, vy = 0, vz = 0, lab = 0;
-  long long cell = 0;
+  int cell = 0;  // x + nx*(y + ny*z); volumes are < 2^31 voxels (validated)
   int gate = 0;
   Real run_w0 = 0;          // float path: weight at the start of the current run
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // per-photon (double path / trace)
@@ -179,7 +191,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
 #pragma unroll
   for (int m = 0; m < (kDet ? kMaxDetMedia : 1); ++m) ppath[m] = 0;
 
-  auto deposit = [&](long long c, int gt, int bvx, int bvy, int bvz, long long q) {
+  auto deposit = [&](int c, int gt, int bvx, int bvy, int bvz, long long q) {
     if (q == 0) return;
     if (A.box_cells) {
       const unsigned ux = static_cast<unsigned>(bvx - A.bx0), uy = static_cast<unsigned>(bvy - A.by0),
@@ -191,7 +203,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         return;
       }
     }
-    atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (c + A.nvox * gt),
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt),
               static_cast<unsigned long long>(q));
   };
   auto quant = [&](Real x) -> long long {
@@ -221,7 +233,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     const Real u = rng.template unit<Real>();
     if constexpr (kF32) {
       // u == 0 (p = 2^-24) stands for the reference's [0, 2^-24) cell: use 2^-25.
-      return -logf(u > 0.0f ? u : 0x1p-25f);
+      return -__logf(u > 0.0f ? u : 0x1p-25f);  // MUFU.LG2: abs. error ~1e-7
     } else {
       return -log(u > 0.0 ? u : 4.9406564584124654e-324);
     }
@@ -310,7 +322,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
               lab = A.lab0;
             }
             set_dir(ux, uy, uz);
-            cell = vx + nx * (vy + static_cast<long long>(ny) * vz);
+            cell = vx + nx * (vy + ny * vz);
             w = Real(1);
             t = Real(0);
             rs = scat_len();
@@ -376,14 +388,11 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     {
       const Real x = M.mua * d;
       Real e;
-      if (x < Real(0.01)) {
-        e = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
+      const Real taylor = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
+      if constexpr (kF32) {
+        e = x < 0.01f ? taylor : __expf(-x);  // branch-free select
       } else {
-        if constexpr (kF32) {
-          e = __expf(-x);
-        } else {
-          e = exp(-x);
-        }
+        e = x < 0.01 ? taylor : exp(-x);
       }
       w1 = w * e;
     }
@@ -431,7 +440,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           ct = Real(2) * xi - Real(1);
         } else {
           if constexpr (kF32) {
-            const float f = M.hg_c / (M.hg_d + M.hg_e * xi);
+            const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
             ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
           } else {
             const double g = M.g;
@@ -443,7 +452,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       }
       Real st;
       if constexpr (kF32) {
-        st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+        st = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
       } else {
         st = sqrt(fmax(0.0, 1.0 - ct * ct));
       }
@@ -546,26 +555,21 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     } else {
       rs = fmax(0.0, rs - d * M.mus);
     }
-    px += dx * d;
-    py += dy * d;
-    pz += dz * d;
     const Real dax = sel3(axis, dx, dy, dz);
     const int stp = dax > Real(0) ? 1 : -1;
-    int nvx = vx, nvy = vy, nvz = vz;
-    long long ncell = cell;
-    if (axis == 0) {
-      px = static_cast<Real>(vx + (stp > 0 ? 1 : 0)) * h;
-      nvx += stp;
-      ncell += stp;
-    } else if (axis == 1) {
-      py = static_cast<Real>(vy + (stp > 0 ? 1 : 0)) * h;
-      nvy += stp;
-      ncell += stp * static_cast<long long>(nx);
-    } else {
-      pz = static_cast<Real>(vz + (stp > 0 ? 1 : 0)) * h;
-      nvz += stp;
-      ncell += stp * nxy;
+    {
+      // land exactly on the crossed plane; the other two coordinates advance
+      const int vax = sel3(axis, vx, vy, vz);
+      const Real plane = static_cast<Real>(vax + (stp > 0 ? 1 : 0)) * h;
+      px = axis == 0 ? plane : px + dx * d;
+      py = axis == 1 ? plane : py + dy * d;
+      pz = axis == 2 ? plane : pz + dz * d;
     }
+    const int nvx = vx + (axis == 0 ? stp : 0);
+    const int nvy = vy + (axis == 1 ? stp : 0);
+    const int nvz = vz + (axis == 2 ? stp : 0);
+    const int stride = axis == 0 ? 1 : (axis == 1 ? nx : nxy32);
+    const int ncell = stp > 0 ? cell + stride : cell - stride;
     const bool exterior = nvx < 0 || nvy < 0 || nvz < 0 || nvx >= nx || nvy >= ny || nvz >= nz;
     const int nlab = exterior ? 0 : static_cast<int>(__ldg(A.labels + ncell));
     const int c1 = M.nclass, c2 = sm_media[nlab].nclass;
@@ -721,7 +725,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         const int by = r % A.bny;
         const int bz = r / A.bny;
         const long long c = (A.bx0 + bx) + nx * ((A.by0 + by) + static_cast<long long>(ny) * (A.bz0 + bz));
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (c + A.nvox * gt), v);
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt), v);
       }
     }
   }

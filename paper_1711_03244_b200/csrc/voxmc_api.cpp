@@ -1,0 +1,447 @@
+// voxmc_api.cpp — the C++ drop-in API (include/voxmc/voxmc.hpp) over the C-ABI.
+//
+// Host bookkeeping restated from the reference (validation rules, presets,
+// FluenceMap arithmetic, partition front-ends); all photon transport goes to
+// the device through vmc_run_range / vmc_run_multi. Error codes from the C-ABI
+// are rethrown as the reference's exception types.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <queue>
+
+#include "vmc.h"
+#include "voxmc/voxmc.hpp"
+
+namespace voxmc {
+
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string msg = vmc_last_error();
+  if (rc == VMC_ERR_VALIDATION) {
+    if (msg.find("outside the voxel grid") != std::string::npos) throw SourceOutsideDomain(msg);
+    throw ValidationError(msg);
+  }
+  throw std::runtime_error(msg);
+}
+
+void check(int rc) {
+  if (rc != VMC_OK) rethrow(rc);
+}
+
+// Flattened scene/config for the C-ABI; owns the arrays the structs point to.
+struct Abi {
+  vmc_scene s{};
+  vmc_config c{};
+  std::vector<double> media, det;
+
+  Abi(const Scene& scene, const SimulationConfig& cfg) {
+    const VoxelGrid& g = scene.grid;
+    s.nx = g.nx();
+    s.ny = g.ny();
+    s.nz = g.nz();
+    s.voxel_mm = g.voxel_size();
+    s.labels = g.labels().data();
+    s.nmedia = static_cast<int32_t>(g.media().size());
+    for (const OpticalProperties& m : g.media()) media.insert(media.end(), {m.mua, m.mus, m.g, m.n});
+    s.media = media.data();
+    const Source& src = scene.source;
+    for (int k = 0; k < 3; ++k) {
+      s.src_pos[k] = src.position[k];
+      s.src_dir[k] = src.direction[k];
+    }
+    s.isotropic = src.isotropic ? 1 : 0;
+    c.photon_count = cfg.photon_count;
+    c.master_seed = cfg.master_seed;
+    c.accumulation_mode =
+        cfg.accumulation_mode == AccumulationMode::SharedAtomic ? VMC_ACCUM_SHARED_ATOMIC : VMC_ACCUM_PRIVATE_MERGE;
+    c.boundary_mode = cfg.boundary_mode == BoundaryMode::ReflectAtMismatch ? VMC_BOUNDARY_REFLECT
+                                                                           : VMC_BOUNDARY_TERMINATE;
+    c.tmax_ns = cfg.tmax_ns;
+    c.roulette_threshold = cfg.roulette_threshold;
+    c.roulette_multiplier = cfg.roulette_multiplier;
+    c.workgroup_size = 0;
+    c.ngates = cfg.ngates;
+    c.precision = cfg.precision == Precision::FP64 ? VMC_PRECISION_FP64 : VMC_PRECISION_FP32;
+    for (const Detector& d : cfg.detectors) det.insert(det.end(), {d.position.x, d.position.y, d.position.z, d.radius});
+    c.ndet = static_cast<int32_t>(cfg.detectors.size());
+    c.det = det.empty() ? nullptr : det.data();
+    c.det_capacity = cfg.det_capacity;
+  }
+};
+
+std::vector<DetectorRecord> unpack_records(const std::vector<unsigned char>& raw, std::uint64_t n, int nmedia) {
+  const std::size_t stride = vmc_det_record_bytes(nmedia);
+  std::vector<DetectorRecord> out(n);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const unsigned char* rec = raw.data() + i * stride;
+    vmc_det_record_head h;
+    std::memcpy(&h, rec, sizeof h);
+    DetectorRecord& r = out[i];
+    r.photon_index = h.photon_index;
+    r.det_id = h.det_id;
+    r.nscat = h.nscat;
+    r.w_exit = h.w_exit;
+    r.t_exit_ns = h.t_exit_ns;
+    r.ppath_mm.resize(static_cast<std::size_t>(std::max(0, nmedia - 1)));
+    std::memcpy(r.ppath_mm.data(), rec + sizeof h, r.ppath_mm.size() * sizeof(float));
+  }
+  return out;
+}
+
+PhotonDisposition from_quanta(const vmc_disposition& d) {
+  return {static_cast<double>(d.deposited_q) * d.quantum, static_cast<double>(d.escaped_q) * d.quantum,
+          static_cast<double>(d.killed_q) * d.quantum, static_cast<double>(d.truncated_q) * d.quantum};
+}
+
+std::vector<vmc_device_profile> profiles(std::span<const DeviceProfile> devs) {
+  std::vector<vmc_device_profile> p(devs.size());
+  for (std::size_t i = 0; i < devs.size(); ++i) p[i] = {devs[i].cores, 0, devs[i].a, devs[i].t0};
+  return p;
+}
+
+}  // namespace
+
+// ---- domain ----------------------------------------------------------------
+VoxelGrid::VoxelGrid(VoxelIndex dims, double voxel_size_mm, std::vector<std::uint8_t> labels,
+                     std::vector<OpticalProperties> media)
+    : dims_(dims), h_(voxel_size_mm), labels_(std::move(labels)), media_(std::move(media)) {
+  if (dims_.x < 1 || dims_.y < 1 || dims_.z < 1) throw ValidationError("VoxelGrid: all dims must be >= 1");
+  if (!(h_ > 0.0)) throw ValidationError("VoxelGrid: voxel_size must be > 0");
+  if (labels_.size() != static_cast<std::size_t>(dims_.x) * dims_.y * dims_.z)
+    throw ValidationError("VoxelGrid: label array size does not match dims");
+  if (media_.empty()) throw ValidationError("VoxelGrid: media list is empty");
+  for (const OpticalProperties& m : media_)
+    if (m.mua < 0.0 || m.mus < 0.0 || m.g < -1.0 || m.g > 1.0 || m.n < 1.0)
+      throw ValidationError("VoxelGrid: invalid optical properties");
+  const std::uint8_t top = labels_.empty() ? 0 : *std::max_element(labels_.begin(), labels_.end());
+  if (top >= media_.size()) throw ValidationError("VoxelGrid: label exceeds media list");
+}
+
+std::optional<VoxelIndex> VoxelGrid::voxel_of(const Vec3& p) const {
+  const VoxelIndex v{static_cast<int>(std::floor(p.x / h_)), static_cast<int>(std::floor(p.y / h_)),
+                     static_cast<int>(std::floor(p.z / h_))};
+  if (!contains(v)) return std::nullopt;
+  return v;
+}
+
+void SimulationConfig::validate() const {
+  if (photon_count < 1) throw ValidationError("photon_count must be >= 1");
+  if (!(tmax_ns > 0.0)) throw ValidationError("tmax must be > 0");
+  if (!(roulette_threshold > 0.0 && roulette_threshold < 1.0))
+    throw ValidationError("roulette_threshold must be in (0, 1)");
+  if (roulette_multiplier < 2) throw ValidationError("roulette_multiplier must be >= 2");
+  if (workgroup_size < 1) throw ValidationError("workgroup_size must be >= 1");
+  if (ngates < 1) throw ValidationError("ngates must be >= 1");
+}
+
+BenchmarkSetup benchmark_preset(Benchmark name) {
+  // 60^3 mm cube of turbid medium, pencil beam at (30,30,0) along +z; B2/B2a
+  // add a 15 mm sphere at the centre and switch to Fresnel boundaries.
+  const bool sphere = name != Benchmark::B1;
+  std::vector<OpticalProperties> media{{0.0, 0.0, 0.0, 1.0}, {0.005, 1.0, 0.01, 1.37}};
+  if (sphere) media.push_back({0.002, 5.0, 0.9, 1.0});
+  std::vector<std::uint8_t> labels(60u * 60u * 60u, 1);
+  if (sphere) {
+    for (int z = 0, i = 0; z < 60; ++z)
+      for (int y = 0; y < 60; ++y)
+        for (int x = 0; x < 60; ++x, ++i) {
+          const double dx = x + 0.5 - 30.0, dy = y + 0.5 - 30.0, dz = z + 0.5 - 30.0;
+          if (dx * dx + dy * dy + dz * dz <= 225.0) labels[i] = 2;
+        }
+  }
+  SimulationConfig cfg;
+  cfg.photon_count = 100'000'000;
+  cfg.boundary_mode = sphere ? BoundaryMode::ReflectAtMismatch : BoundaryMode::TerminateAtBoundary;
+  cfg.accumulation_mode = name == Benchmark::B2a ? AccumulationMode::SharedAtomic : AccumulationMode::PrivateMerge;
+  Source src;
+  src.position = {30.0, 30.0, 0.0};
+  return BenchmarkSetup{VoxelGrid({60, 60, 60}, 1.0, std::move(labels), std::move(media)), src, cfg};
+}
+
+std::optional<Benchmark> benchmark_from_name(std::string_view n) {
+  if (n == "B1" || n == "b1") return Benchmark::B1;
+  if (n == "B2" || n == "b2") return Benchmark::B2;
+  if (n == "B2a" || n == "b2a" || n == "B2A") return Benchmark::B2a;
+  return std::nullopt;
+}
+
+std::string_view benchmark_name(Benchmark b) {
+  return b == Benchmark::B1 ? "B1" : (b == Benchmark::B2 ? "B2" : "B2a");
+}
+
+std::uint64_t mix64(std::uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+RngStream::RngStream(std::uint64_t master_seed, std::uint64_t stream_id) : id_(stream_id) {
+  const std::uint64_t z = master_seed ^ stream_id;
+  s_[0] = mix64(z);
+  s_[1] = mix64(z + 0x9E3779B97F4A7C15ULL);
+  if ((s_[0] | s_[1]) == 0) s_[1] = 0x6A09E667F3BCC909ULL;
+}
+
+double hg_cos_theta(double g, double xi) {
+  if (std::fabs(g) < 1e-6) return 2.0 * xi - 1.0;
+  const double f = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
+  return std::clamp((1.0 + g * g - f * f) / (2.0 * g), -1.0, 1.0);
+}
+
+double fresnel_reflectance(double n1, double n2, double ci) {
+  ci = std::clamp(ci, 0.0, 1.0);
+  const double eta = n1 / n2;
+  const double st2 = eta * eta * (1.0 - ci * ci);
+  if (st2 > 1.0) return 1.0;
+  const double ct = std::sqrt(1.0 - st2);
+  const double rs = (n1 * ci - n2 * ct) / (n1 * ci + n2 * ct);
+  const double rp = (n1 * ct - n2 * ci) / (n1 * ct + n2 * ci);
+  return 0.5 * (rs * rs + rp * rp);
+}
+
+// ---- FluenceMap -------------------------------------------------------------
+FluenceMap::FluenceMap(VoxelIndex dims, std::uint64_t photon_count, AccumulationMode mode, bool track_counts,
+                       int ngates)
+    : dims_(dims), photon_count_(photon_count), mode_(mode), quantum_(vmc_quantum_for(photon_count)),
+      ngates_(ngates) {
+  if (dims.x < 1 || dims.y < 1 || dims.z < 1) throw ValidationError("FluenceMap: dims must be >= 1");
+  if (photon_count < 1) throw ValidationError("FluenceMap: photon_count must be >= 1");
+  if (ngates < 1) throw ValidationError("FluenceMap: ngates must be >= 1");
+  cells_.assign(voxel_count() * static_cast<std::size_t>(ngates), 0);
+  if (track_counts) counts_.assign(voxel_count(), 0);
+}
+
+void FluenceMap::deposit(std::size_t cell, double dw) {
+  const auto q = static_cast<std::int64_t>(std::llround(dw / quantum_));
+  if (mode_ == AccumulationMode::SharedAtomic) {
+    std::atomic_ref<std::int64_t>(cells_[cell]).fetch_add(q, std::memory_order_relaxed);
+    if (!counts_.empty()) std::atomic_ref<std::int64_t>(counts_[cell]).fetch_add(1, std::memory_order_relaxed);
+  } else {
+    cells_[cell] += q;
+    if (!counts_.empty()) ++counts_[cell];
+  }
+}
+
+void FluenceMap::deposit(const VoxelIndex& v, double dw) {
+  if (v.x < 0 || v.y < 0 || v.z < 0 || v.x >= dims_.x || v.y >= dims_.y || v.z >= dims_.z)
+    throw VoxelOutOfRange("deposit: voxel outside map");
+  if (dw < 0.0) throw ValidationError("deposit: negative weight");
+  deposit(static_cast<std::size_t>(v.x) + static_cast<std::size_t>(dims_.x) * (v.y + static_cast<std::size_t>(dims_.y) * v.z), dw);
+}
+
+std::int64_t FluenceMap::raw_cell(std::size_t cell) const {
+  std::int64_t s = 0;
+  for (int g = 0; g < ngates_; ++g) s += cells_[static_cast<std::size_t>(g) * voxel_count() + cell];
+  return s;
+}
+
+double FluenceMap::value(std::size_t cell) const {
+  return normalized_ ? values_[cell] : static_cast<double>(raw_cell(cell)) * quantum_;
+}
+
+double FluenceMap::total_deposited() const {
+  const std::int64_t s = std::accumulate(cells_.begin(), cells_.end(), std::int64_t{0});
+  return static_cast<double>(s) * quantum_;
+}
+
+void FluenceMap::add(const FluenceMap& o) {
+  if (o.dims_ != dims_ || o.ngates_ != ngates_) throw DimensionMismatch("FluenceMap::add: dims differ");
+  if (o.quantum_ != quantum_) throw DimensionMismatch("FluenceMap::add: quantum differs");
+  if (normalized_ || o.normalized_) throw AlreadyNormalized("FluenceMap::add: normalized map");
+  for (std::size_t i = 0; i < cells_.size(); ++i) cells_[i] += o.cells_[i];
+  if (!counts_.empty() && !o.counts_.empty())
+    for (std::size_t i = 0; i < counts_.size(); ++i) counts_[i] += o.counts_[i];
+}
+
+void FluenceMap::normalize(const VoxelGrid& grid) {
+  if (normalized_) throw AlreadyNormalized("FluenceMap::normalize: already normalized");
+  if (grid.dims() != dims_) throw DimensionMismatch("FluenceMap::normalize: grid dims differ");
+  const double vol = grid.voxel_size() * grid.voxel_size() * grid.voxel_size();
+  values_.assign(voxel_count(), 0.0);
+  zero_mua_voxels_ = 0;
+  for (std::size_t i = 0; i < voxel_count(); ++i) {
+    const double mua = grid.medium(grid.labels()[i]).mua;
+    if (mua > 0.0)
+      values_[i] = static_cast<double>(raw_cell(i)) * quantum_ / (mua * vol * static_cast<double>(photon_count_));
+    else
+      ++zero_mua_voxels_;
+  }
+  normalized_ = true;
+}
+
+std::vector<float> FluenceMap::to_float_volume() const {
+  std::vector<float> v(voxel_count());
+  for (std::size_t i = 0; i < v.size(); ++i) v[i] = static_cast<float>(value(i));
+  return v;
+}
+
+FluenceMap merge(std::span<const FluenceMap> maps) {
+  if (maps.empty()) throw DimensionMismatch("merge: empty map list");
+  FluenceMap out(maps[0].dims(), maps[0].photon_count(), AccumulationMode::PrivateMerge,
+                 maps[0].deposit_count(0) >= 0, maps[0].ngates());
+  for (const FluenceMap& m : maps) out.add(m);
+  return out;
+}
+
+// ---- scheduler --------------------------------------------------------------
+std::uint64_t Partition::total() const { return std::accumulate(counts.begin(), counts.end(), std::uint64_t{0}); }
+
+std::optional<Strategy> strategy_from_name(std::string_view n) {
+  if (n == "s1" || n == "S1") return Strategy::S1;
+  if (n == "s2" || n == "S2") return Strategy::S2;
+  if (n == "s3" || n == "S3") return Strategy::S3;
+  return std::nullopt;
+}
+
+std::string_view strategy_name(Strategy s) { return s == Strategy::S1 ? "s1" : (s == Strategy::S2 ? "s2" : "s3"); }
+
+int thread_count_heuristic(int cores, int per_core) {
+  if (cores < 1 || per_core < 1) throw ValidationError("thread_count_heuristic: arguments must be >= 1");
+  return cores * per_core;
+}
+
+Partition make_partition(std::uint64_t total, std::span<const DeviceProfile> devices, Strategy s) {
+  if (devices.empty()) throw ValidationError("partition: no devices");
+  const auto p = profiles(devices);
+  Partition out;
+  out.counts.assign(devices.size(), 0);
+  const int code = s == Strategy::S1 ? VMC_STRATEGY_S1 : (s == Strategy::S2 ? VMC_STRATEGY_S2 : VMC_STRATEGY_S3);
+  check(vmc_partition(code, total, static_cast<int>(devices.size()), p.data(), out.counts.data()));
+  return out;
+}
+
+Partition partition_s1(std::uint64_t t, std::span<const DeviceProfile> d) { return make_partition(t, d, Strategy::S1); }
+Partition partition_s2(std::uint64_t t, std::span<const DeviceProfile> d) { return make_partition(t, d, Strategy::S2); }
+Partition partition_s3(std::uint64_t t, std::span<const DeviceProfile> d) { return make_partition(t, d, Strategy::S3); }
+
+double model_makespan(const Partition& p, std::span<const DeviceProfile> devices) {
+  const auto pr = profiles(devices);
+  const int n = static_cast<int>(std::min(p.counts.size(), devices.size()));
+  return vmc_model_makespan(n, p.counts.data(), pr.data());
+}
+
+GroupRunResult run_group_on(int gpu, std::uint64_t first_index, std::uint64_t quota, const Scene& scene,
+                            const SimulationConfig& config) {
+  config.validate();
+  Abi abi(scene, config);
+  FluenceMap map(scene.grid.dims(), config.photon_count, config.accumulation_mode, false, config.ngates);
+  vmc_disposition tot{};
+  const int nm = static_cast<int>(scene.grid.media().size());
+  std::vector<unsigned char> det(config.detectors.empty() ? 0 : config.det_capacity * vmc_det_record_bytes(nm));
+  std::uint64_t ndet = 0;
+  double ms = 0.0;
+  check(vmc_run_range(&abi.s, &abi.c, first_index, quota, gpu, map.raw_cells().data(), &tot,
+                      det.empty() ? nullptr : det.data(), &ndet, &ms));
+  GroupRunResult r{std::move(map), from_quanta(tot), {quota}, ms, {}, ndet};
+  if (!config.detectors.empty()) r.detections = unpack_records(det, std::min(ndet, config.det_capacity), nm);
+  return r;
+}
+
+GroupRunResult run_group_dynamic(std::uint64_t first_index, std::uint64_t quota, int threads, const Scene& scene,
+                                 const SimulationConfig& config) {
+  if (threads < 1) throw ValidationError("run_group: threads must be >= 1");
+  GroupRunResult r = run_group_on(0, first_index, quota, scene, config);
+  // one device worker pool: the whole quota is reported in slot 0
+  r.per_thread_photons.assign(static_cast<std::size_t>(threads), 0);
+  r.per_thread_photons[0] = quota;
+  return r;
+}
+
+GroupRunResult run_static_split(std::uint64_t first_index, std::uint64_t quota, int threads, const Scene& scene,
+                                const SimulationConfig& config) {
+  // per-photon streams make static and dynamic claiming bit-identical
+  return run_group_dynamic(first_index, quota, threads, scene, config);
+}
+
+double static_split_makespan(std::span<const double> costs, int threads) {
+  if (threads < 1) throw ValidationError("threads must be >= 1");
+  const std::size_t block = (costs.size() + threads - 1) / threads;
+  double worst = 0.0;
+  for (std::size_t b = 0; b < costs.size(); b += block)
+    worst = std::max(worst, std::accumulate(costs.begin() + b, costs.begin() + std::min(costs.size(), b + block), 0.0));
+  return worst;
+}
+
+double dynamic_makespan(std::span<const double> costs, int threads) {
+  if (threads < 1) throw ValidationError("threads must be >= 1");
+  std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+  for (int t = 0; t < threads; ++t) free_at.push(0.0);
+  double worst = 0.0;
+  for (double c : costs) {
+    const double done = free_at.top() + c;
+    free_at.pop();
+    free_at.push(done);
+    worst = std::max(worst, done);
+  }
+  return worst;
+}
+
+Calibration calibrate(const DeviceProfile& device, std::uint64_t n1, std::uint64_t n2, const Scene& scene,
+                      const SimulationConfig& config, int threads, std::uint64_t noise_seed) {
+  if (!(n2 > n1 && n1 >= 1)) throw ValidationError("calibrate: need n2 > n1 >= 1");
+  double t1, t2;
+  if (device.kind == DeviceKind::CudaGpu) {
+    SimulationConfig pilot = config;
+    pilot.photon_count = n2;
+    t1 = run_group_on(device.gpu, 0, n1, scene, pilot).wall_ms;
+    t2 = run_group_on(device.gpu, 0, n2, scene, pilot).wall_ms;
+  } else if (device.kind == DeviceKind::Simulated) {
+    t1 = device.a * static_cast<double>(n1) + device.t0;
+    t2 = device.a * static_cast<double>(n2) + device.t0;
+    if (device.jitter_sigma > 0.0) {
+      RngStream noise(noise_seed, 0x706c6f74);
+      auto factor = [&] {
+        const double u1 = std::max(noise.next_unit(), 1e-300), u2 = noise.next_unit();
+        return std::exp(device.jitter_sigma * std::sqrt(-2.0 * std::log(u1)) *
+                        std::cos(2.0 * 3.14159265358979323846 * u2));
+      };
+      t1 *= factor();
+      t2 *= factor();
+    }
+  } else {
+    throw ValidationError("calibrate: host worker pools are not executed by the B200 library");
+  }
+  (void)threads;
+  if (t2 <= t1) throw NonPositiveSlope("calibrate: T2 <= T1; increase n2 or rerun");
+  Calibration c;
+  c.a = (t2 - t1) / static_cast<double>(n2 - n1);
+  c.t0 = std::max(0.0, t1 - c.a * static_cast<double>(n1));
+  return c;
+}
+
+MultiDeviceResult run_multi_device(std::uint64_t total, std::span<const DeviceProfile> devices, Strategy strategy,
+                                   const Scene& scene, const SimulationConfig& config, int threads_per_device) {
+  (void)threads_per_device;
+  if (devices.empty()) throw ValidationError("run_multi_device: no devices");
+  for (const DeviceProfile& d : devices)
+    if (d.kind != DeviceKind::CudaGpu) throw ValidationError("run_multi_device: devices must be DeviceKind::CudaGpu");
+  Partition part = make_partition(total, devices, strategy);
+  SimulationConfig cfg = config;
+  cfg.photon_count = total;  // shared quantum (reference scheduler.cpp:412-413)
+  cfg.validate();
+  Abi abi(scene, cfg);
+  FluenceMap map(scene.grid.dims(), total, AccumulationMode::PrivateMerge, false, cfg.ngates);
+  std::vector<int> gpus;
+  for (const DeviceProfile& d : devices) gpus.push_back(d.gpu);
+  vmc_disposition tot{};
+  const int nm = static_cast<int>(scene.grid.media().size());
+  std::vector<unsigned char> det(cfg.detectors.empty() ? 0 : cfg.det_capacity * vmc_det_record_bytes(nm));
+  std::uint64_t ndet = 0;
+  std::vector<double> ms(devices.size(), 0.0);
+  double red = 0.0;
+  check(vmc_run_multi(&abi.s, &abi.c, static_cast<int>(devices.size()), gpus.data(), part.counts.data(),
+                      map.raw_cells().data(), &tot, det.empty() ? nullptr : det.data(), &ndet, ms.data(), &red));
+  MultiDeviceResult r{std::move(map), from_quanta(tot), part, {}, 0.0, red, {}, ndet};
+  for (std::size_t i = 0; i < devices.size(); ++i) {
+    r.devices.push_back({devices[i].name, part.counts[i], part.counts[i] ? ms[i] : 0.0});
+    r.makespan_ms = std::max(r.makespan_ms, r.devices.back().wall_ms);
+  }
+  r.makespan_ms += red;
+  if (!cfg.detectors.empty()) r.detections = unpack_records(det, std::min(ndet, cfg.det_capacity), nm);
+  return r;
+}
+
+}  // namespace voxmc
