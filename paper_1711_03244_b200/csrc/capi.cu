@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -78,6 +79,11 @@ int bit_width_u64(uint64_t v) {
 // FluenceMap quantum rule (proj/core/src/fluence.cpp:11-14): power-of-two
 // quantum so N unit-weight photons cannot overflow 63 bits.
 int quantum_bits(uint64_t n) { return 62 - bit_width_u64(n | 1u); }
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
 
 struct HostLaunch {
   double dir[3];
@@ -333,7 +339,14 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
     A.bny = n[1];
     A.bnz = n[2];
     A.box_cells = side >= 4 ? n[0] * n[1] * n[2] * c->ngates : 0;
+    // Measured on B200: L2 atomics absorb the source hot spot (<= 2e8 adds/s on one
+    // cell) and the box's extra address math costs more than it saves, so it is
+    // off unless VMC_HOTBOX=1.
+    const char* env = std::getenv("VMC_HOTBOX");
+    if (!(env && env[0] == '1')) A.box_cells = 0;
   }
+  A.scatter_pct = env_int("VMC_SCATTER_PCT", 50);
+  A.refill_min = env_int("VMC_REFILL_MIN", 2);
   A.ndet = c->ndet;
   A.nppath = std::max(0, s->nmedia - 1);
   A.rec_stride = static_cast<int>(P->rec_stride);

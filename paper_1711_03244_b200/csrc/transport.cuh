@@ -79,6 +79,9 @@ struct KernelArgs {
   int bx0, by0, bz0, bnx, bny, bnz, box_cells, pad2;
   // detectors
   int ndet, nppath, rec_stride, pad3;
+  // warp scheduling: scatter phase when >= scatter_pct % of live lanes wait;
+  // refill when >= refill_min lanes are empty
+  int scatter_pct, refill_min;
   double det[kMaxDet][4];
   unsigned char* det_out;
   unsigned long long* det_count;
@@ -173,7 +176,9 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   long long acc_dep = 0, acc_esc = 0, acc_kill = 0, acc_trunc = 0;
 
   // photon state
-  bool alive = false;
+  // 0 = ready to step, 1 = at a scattering point (scatter deferred to a scatter
+  // phase), 2 = no photon (lane waits for a refill)
+  int phase = 2;
   bool exhausted = false;  // warp-uniform: counter ran past `count`
   uint64_t idx = 0;
   Rng rng;
@@ -258,19 +263,25 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       acc_kill += llround(pd_kill * A.qscale);
       acc_trunc += llround(pd_trunc * A.qscale);
     }
-    alive = false;
+    phase = 2;
   };
 
   for (;;) {
     // ---- refill dead lanes: one atomicAdd per warp (dynamic claiming) ----
-    if (!exhausted) {
-      const unsigned need = __ballot_sync(0xffffffffu, !alive);
-      if (need) {
+    // Warp-level phase scheduler. Photons are independent, so the order in
+    // which a warp interleaves their events never changes any photon's
+    // arithmetic or RNG sequence; it only decides which lanes run together.
+    // A scatter is deferred until it can run with at least half of the
+    // working lanes; dead lanes are refilled in groups of kRefillMin.
+    unsigned dead = __ballot_sync(0xffffffffu, phase == 2);
+    if (!exhausted && dead && (__popc(dead) >= A.refill_min || dead == 0xffffffffu)) {
+      const unsigned need = dead;
+      {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(A.claim, static_cast<unsigned long long>(__popc(need)));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base + __popc(need) >= A.count) exhausted = true;
-        if (!alive) {
+        if (phase == 2) {
           const unsigned long long my = base + __popc(need & lanemask_lt);
           if (my < A.count) {
             // ---- launch, transport.cpp:83-106 ----
@@ -334,14 +345,18 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
 #pragma unroll
               for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] = 0;
             }
-            alive = true;
+            phase = 0;
           }
         }
       }
+      dead = __ballot_sync(0xffffffffu, phase == 2);
     }
-    if (!__any_sync(0xffffffffu, alive)) break;
-    if (!alive) continue;
-
+    if (dead == 0xffffffffu) {
+      if (exhausted) break;
+      continue;
+    }
+    do {  // ---- step phase: every lane holding a photon that is not at a scattering point
+    if (phase != 0) break;
     // ---- one advance() step, transport.cpp:161-225 ----
     const Medium<Real>& M = sm_media[lab];
     if constexpr (kTrace) ++steps;
@@ -424,118 +439,13 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       }
       pd_trunc += w;
       finish(2);
-      continue;
+      break;
     }
 
-    if (d_s <= d_b) {
-      // ---- scatter: move, hg_scatter (transport.cpp:126-147), new length ----
+    if (d_s <= d_b) {  // StepKind::Scattered: move to the scattering point
       px += dx * d;
       py += dy * d;
       pz += dz * d;
-      if constexpr (kTrace || kDet) ++nscat;
-      Real ct;
-      {
-        const Real xi = rng.template unit<Real>();
-        if (M.iso) {
-          ct = Real(2) * xi - Real(1);
-        } else {
-          if constexpr (kF32) {
-            const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
-            ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
-          } else {
-            const double g = M.g;
-            const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
-            ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
-            ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
-          }
-        }
-      }
-      Real st;
-      if constexpr (kF32) {
-        st = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
-      } else {
-        st = sqrt(fmax(0.0, 1.0 - ct * ct));
-      }
-      Real cp, sp;
-      for (;;) {  // sample_azimuth, transport.cpp:32-44
-        const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
-        const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
-        const Real r2 = ax_ * ax_ + ay_ * ay_;
-        if (r2 > Real(1e-12) && r2 <= Real(1)) {
-          Real k;
-          if constexpr (kF32) {
-            k = rsqrtf(r2);
-          } else {
-            k = 1.0 / sqrt(r2);
-          }
-          cp = ax_ * k;
-          sp = ay_ * k;
-          break;
-        }
-      }
-      Real ox, oy, oz;
-      if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
-        ox = st * cp;
-        oy = st * sp;
-        oz = dz > Real(0) ? ct : -ct;
-      } else {
-        if constexpr (kF32) {
-          const float one_m = 1.0f - dz * dz;
-          const float rden = rsqrtf(one_m);
-          const float den = one_m * rden;
-          const float sr = st * rden;
-          ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
-          oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
-          oz = -st * cp * den + dz * ct;
-        } else {
-          const double den = sqrt(1.0 - dz * dz);
-          ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
-          oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
-          oz = -st * cp * den + dz * ct;
-        }
-      }
-      {
-        const Real n2 = ox * ox + oy * oy + oz * oz;
-        if constexpr (kF32) {
-          if (fabsf(n2 - 1.0f) > 1e-6f) {
-            const float k = rsqrtf(n2);
-            ox *= k;
-            oy *= k;
-            oz *= k;
-          }
-        } else {
-          if (fabs(n2 - 1.0) > 1e-12) {
-            const double k = 1.0 / sqrt(n2);
-            ox *= k;
-            oy *= k;
-            oz *= k;
-          }
-        }
-      }
-      set_dir(ox, oy, oz);
-      rs = scat_len();
-      // roulette after a scatter only (transport.cpp:333-343, 300-306)
-      if (w < rthr) {
-        const Real before = w;
-        const bool survive = rng.template unit<Real>() < inv_rmult;
-        if constexpr (kF32) {
-          const long long q = quant(run_w0 - w);
-          deposit(cell, gate, vx, vy, vz, q);
-          acc_dep += q;
-        }
-        if (!survive) {
-          if constexpr (kF32) acc_kill += quant(before);
-          pd_kill += before;
-          finish(1);
-          continue;
-        }
-        w *= rmult;
-        if constexpr (kF32) {
-          acc_kill += quant(before) - quant(w);
-          run_w0 = w;
-        }
-        pd_kill += before - w;
-      }
       if constexpr (kGates && kF32) {
         const int ng = gate_of(t);
         if (ng != gate) {
@@ -546,7 +456,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           gate = ng;
         }
       }
-      continue;
+      phase = 1;  // hg_scatter + new length + roulette run in a scatter phase
+      break;
     }
 
     // ---- land exactly on the face (transport.cpp:197-211) ----
@@ -667,7 +578,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         }
       }
       finish(0);
-      continue;
+      break;
     }
     if (move) {
       if constexpr (kF32) {
@@ -692,6 +603,127 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         acc_dep += q;
         run_w0 = w;
         gate = ng;
+      }
+    }
+    } while (0);
+    // ---- scatter phase: run the deferred scatters once at least half of the
+    // lanes holding a photon are at a scattering point (or nobody can step) ----
+    {
+      const unsigned pend = __ballot_sync(0xffffffffu, phase == 1);
+      const unsigned live = ~__ballot_sync(0xffffffffu, phase == 2);
+      if (pend != 0u && (pend == live || 100 * __popc(pend) >= A.scatter_pct * __popc(live))) {
+      if (phase == 1) {
+          {
+          // ---- scatter: hg_scatter (transport.cpp:126-147), new length ----
+          const Medium<Real>& M = sm_media[lab];
+          phase = 0;
+          if constexpr (kTrace || kDet) ++nscat;
+          Real ct;
+          {
+            const Real xi = rng.template unit<Real>();
+            if (M.iso) {
+              ct = Real(2) * xi - Real(1);
+            } else {
+              if constexpr (kF32) {
+                const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
+                ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
+              } else {
+                const double g = M.g;
+                const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
+                ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
+                ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
+              }
+            }
+          }
+          Real st;
+          if constexpr (kF32) {
+            st = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
+          } else {
+            st = sqrt(fmax(0.0, 1.0 - ct * ct));
+          }
+          Real cp, sp;
+          for (;;) {  // sample_azimuth, transport.cpp:32-44
+            const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
+            const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
+            const Real r2 = ax_ * ax_ + ay_ * ay_;
+            if (r2 > Real(1e-12) && r2 <= Real(1)) {
+              Real k;
+              if constexpr (kF32) {
+                k = rsqrtf(r2);
+              } else {
+                k = 1.0 / sqrt(r2);
+              }
+              cp = ax_ * k;
+              sp = ay_ * k;
+              break;
+            }
+          }
+          Real ox, oy, oz;
+          if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
+            ox = st * cp;
+            oy = st * sp;
+            oz = dz > Real(0) ? ct : -ct;
+          } else {
+            if constexpr (kF32) {
+              const float one_m = 1.0f - dz * dz;
+              const float rden = rsqrtf(one_m);
+              const float den = one_m * rden;
+              const float sr = st * rden;
+              ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
+              oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
+              oz = -st * cp * den + dz * ct;
+            } else {
+              const double den = sqrt(1.0 - dz * dz);
+              ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
+              oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
+              oz = -st * cp * den + dz * ct;
+            }
+          }
+          {
+            const Real n2 = ox * ox + oy * oy + oz * oz;
+            if constexpr (kF32) {
+              if (fabsf(n2 - 1.0f) > 1e-6f) {
+                const float k = rsqrtf(n2);
+                ox *= k;
+                oy *= k;
+                oz *= k;
+              }
+            } else {
+              if (fabs(n2 - 1.0) > 1e-12) {
+                const double k = 1.0 / sqrt(n2);
+                ox *= k;
+                oy *= k;
+                oz *= k;
+              }
+            }
+          }
+          set_dir(ox, oy, oz);
+          rs = scat_len();
+          // roulette after a scatter only (transport.cpp:333-343, 300-306)
+          if (w < rthr) {
+            const Real before = w;
+            const bool survive = rng.template unit<Real>() < inv_rmult;
+            if constexpr (kF32) {
+              const long long q = quant(run_w0 - w);
+              deposit(cell, gate, vx, vy, vz, q);
+              acc_dep += q;
+            }
+            if (!survive) {
+              if constexpr (kF32) acc_kill += quant(before);
+              pd_kill += before;
+              finish(1);
+            } else {
+            w *= rmult;
+            if constexpr (kF32) {
+              acc_kill += quant(before) - quant(w);
+              run_w0 = w;
+            }
+            pd_kill += before - w;
+            }
+          }
+          }
+
+      }
       }
     }
   }

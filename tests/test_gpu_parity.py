@@ -10,6 +10,8 @@ Gates, same master_seed and photon indices on both sides:
   energy audit   |deposited+escaped+killed+truncated - N| / N <= 1e-6 (config.cpp:316-319)
   determinism    integer maps bit-identical across reruns and across range splits
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -96,15 +98,22 @@ def test_run_parity(gpu, ref, golden, name, tol):
 
 
 def test_fp64_run_parity(gpu, ref):
+    import oracle
     st = setup("b2", n=100_000)
     st.config.precision = v.Precision.FP64
     g = gpu.run_group_dynamic(0, 100_000, 1, st.scene, st.config)
     w = ref.walk(st.scene, st.config, 0, 100_000, threads=8)
     assert g.totals.deposited / w["disp"][0] - 1 == pytest.approx(0, abs=1e-6)
     cw = g.map.cw_cells()
-    # per-step llround deposits: most cells are bit-identical to the reference
-    assert (cw == w["cells"]).mean() > 0.5
     assert l2_rel(cw, w["cells"], w["cells"] > 0) < 1e-5
+    # against the reference built without FMA contraction (as the FP64 kernel is
+    # compiled) the per-step llround deposits differ only through libm-vs-CUDA
+    # log() rounding: most touched cells are bit-identical
+    r0 = oracle.RefLib(os.path.join(oracle.HERE, "_ref", "libvoxmc_ref_nofma.so"))
+    c0, d0, _ = r0.run_group(st.scene, st.config, 0, 100_000, 8)
+    touched = c0 > 0
+    assert (cw[touched] == c0[touched]).mean() > 0.5
+    assert l2_rel(cw, c0, touched) < 1e-6
 
 
 def test_determinism_and_range_split(gpu):
