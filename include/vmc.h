@@ -215,6 +215,17 @@ VMC_API int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, i
  * host array out[count]. Deposits are not accumulated. Synchronous. */
 VMC_API int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_photon_trace* out);
 
+/* K4: fluence normalization Phi = E / (mua * V * N) (reference FluenceMap::normalize,
+ * fluence.cpp:62-84, and to_float_volume, :86-90) as one device pass. d_cells as
+ * written by vmc_plan_run ([ngates][z][y][x]); d_out float [ngates * V] when
+ * sum_gates == 0, else [V] (CW, gate-summed before normalizing). Voxels with
+ * mua == 0 map to 0. normalized == 0 skips the division (raw weight = cell * quantum). */
+VMC_API int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t photon_count, float* d_out,
+                               int sum_gates, int normalized, void* stream);
+
+/* FNV-1a 64 of a byte buffer (the reference's volume checksum, volume_io.cpp:13-20). Host only. */
+VMC_API uint64_t vmc_fnv1a64(const void* data, size_t bytes);
+
 /* Number of kernels vmc_plan_run enqueues per call (for launch accounting). */
 VMC_API int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags);
 

@@ -26,14 +26,14 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 
 # (source, object, extra flags)
 UNITS = [
-    ("transport_kernels.cu", "transport_f32.o", ["-DVMC_REAL=float"]),
+    ("transport_kernels.cu", "transport_f32.o", ["-DVMC_REAL=float", "-DVMC_REAL_IS_FLOAT=1"]),
     ("transport_kernels.cu", "transport_f64.o", ["-DVMC_REAL=double", "--fmad=false"]),
     ("capi.cu", "capi.o", []),
     ("partition.cpp", "partition.o", []),
     ("voxmc_api.cpp", "voxmc_api.o", []),
 ]
 
-HEADERS = ["transport.cuh", "rng.cuh", "partition.hpp"]
+HEADERS = ["transport.cuh", "transport_pool.cuh", "rng.cuh", "partition.hpp"]
 
 
 def _stale(obj: str, src: str) -> bool:

@@ -29,6 +29,8 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace);
 const void* transport_kernel_double(bool gates, bool det, bool trace);
+const void* transport_kernel_pool(bool gates, bool det, bool trace);
+int pool_smem_bytes(bool det, bool trace);
 }  // namespace vmc
 
 namespace {
@@ -234,11 +236,13 @@ struct vmc_plan {
   int nx = 0, ny = 0, nz = 0, nmedia = 0;
   uint64_t ncells = 0;
   size_t rec_stride = 0;
-  DevBuf labels, media, claim, err;
+  DevBuf labels, media, claim, err, mua;
+  double voxel_mm = 1.0;
   vmc::KernelArgs args{};
   int sms = 0;
   int block = vmc::kBlock;
-  size_t smem = 0;
+  size_t smem = 0, smem_trace = 0;
+  bool pool = false;
   int grid = 0, grid_trace = 0;
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
@@ -278,6 +282,13 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
     P->media.alloc(media_bytes, device);
     ck(cudaMemcpy(P->media.p, m.data(), media_bytes, cudaMemcpyHostToDevice), "upload media");
   }
+  {
+    std::vector<double> mua(static_cast<size_t>(s->nmedia));
+    for (int m = 0; m < s->nmedia; ++m) mua[m] = s->media[4 * m];
+    P->mua.alloc(mua.size() * sizeof(double), device);
+    ck(cudaMemcpy(P->mua.p, mua.data(), mua.size() * sizeof(double), cudaMemcpyHostToDevice), "upload mua");
+  }
+  P->voxel_mm = s->voxel_mm;
   P->claim.alloc(sizeof(unsigned long long), device);
   P->err.alloc(sizeof(int), device);
   ck(cudaMemset(P->err.p, 0, sizeof(int)), "cudaMemset");
@@ -355,18 +366,33 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.det_cap = c->det_capacity;
 
   const bool gates = c->ngates > 1, det = c->ndet > 0;
-  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
-  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
-  P->smem = media_bytes + static_cast<size_t>(A.box_cells) * 8;
-  ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-  if (P->smem > 48 * 1024) {
-    ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
-    ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+  // FP32 product path: K1 v2 (per-warp photon pool); VMC_KERNEL=v1 selects the
+  // register-resident v1 kernel (kept for comparison). FP64 parity: v1<double>.
+  const char* kv = std::getenv("VMC_KERNEL");
+  P->pool = !f64 && !(kv && std::strcmp(kv, "v1") == 0);
+  if (P->pool) {
+    A.box_cells = 0;
+    A.scatter_pct = env_int("VMC_POOL_SCATTER_PCT", 100);
+    A.refill_min = env_int("VMC_POOL_REFILL_MIN", 8);
+    P->kern = vmc::transport_kernel_pool(gates, det, false);
+    P->kern_trace = vmc::transport_kernel_pool(gates, det, true);
+    const size_t mb = (media_bytes + 15) & ~static_cast<size_t>(15);
+    P->smem = mb + static_cast<size_t>(vmc::pool_smem_bytes(det, false));
+    P->smem_trace = mb + static_cast<size_t>(vmc::pool_smem_bytes(det, true));
+  } else {
+    P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
+    P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
+    P->smem = media_bytes + static_cast<size_t>(A.box_cells) * 8;
+    P->smem_trace = P->smem;
   }
+  ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+  ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem_trace)),
+     "smem attr");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern, P->block, P->smem), "occupancy");
   P->grid = std::max(1, per_sm) * P->sms;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern_trace, P->block, P->smem), "occupancy");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern_trace, P->block, P->smem_trace), "occupancy");
   P->grid_trace = std::max(1, per_sm) * P->sms;
 }
 
@@ -395,10 +421,18 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   A.trace = d_trace;
   void* argv[] = {&A};
   // never launch more persistent threads than photons need
+  if (P->pool && count > 0xffffffffull) {
+    // the pool keeps the photon offset in 32 bits: split very large ranges
+    for (uint64_t off = 0; off < count; off += 0x80000000ull)
+      plan_enqueue(P, first + off, std::min<uint64_t>(0x80000000ull, count - off), d_cells, d_totals, d_det,
+                   d_det_count, st, 0u, trace, d_trace ? d_trace + off : nullptr);
+    return;
+  }
   const uint64_t need_blocks = (count + P->block - 1) / P->block;
   const int full = trace ? P->grid_trace : P->grid;
   const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));
-  ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv, P->smem, st),
+  ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv,
+                      trace ? P->smem_trace : P->smem, st),
      "launch transport");
 }
 
@@ -532,6 +566,30 @@ constexpr int kNcclSum = 0;    // ncclSum
 }  // namespace
 
 namespace {
+// K4: normalize (fluence.cpp:62-90). One thread per output cell; labels via
+// the read-only path, mua from a small constant-size table argument.
+__global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* __restrict__ labels,
+                            const double* __restrict__ mua, long long nvox, int ngates, int sum_gates,
+                            int normalized, double scale, float* __restrict__ out) {
+  const long long n = sum_gates ? nvox : nvox * ngates;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long v = i % nvox;
+    long long raw = 0;
+    if (sum_gates) {
+      for (int g = 0; g < ngates; ++g) raw += cells[v + g * nvox];
+    } else {
+      raw = cells[i];
+    }
+    double val = static_cast<double>(raw) * scale;  // scale = quantum (/(V N) when normalized)
+    if (normalized) {
+      const double m = mua[__ldg(labels + v)];
+      val = m > 0.0 ? val / m : 0.0;
+    }
+    out[i] = static_cast<float>(val);
+  }
+}
+
 __global__ void k_rng_kat(uint64_t seed, uint64_t stream, int n, uint64_t* out) {
   vmc::Xs128p<false> r;
   r.seed(seed, stream);
@@ -806,6 +864,35 @@ int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_pho
     if (count) ck(cudaMemcpy(out, tr.p, count * sizeof(vmc_photon_trace), cudaMemcpyDeviceToHost), "download trace");
     check_launch_errors(plan);
   });
+}
+
+int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t photon_count, float* d_out, int sum_gates,
+                       int normalized, void* stream) {
+  return guarded([&] {
+    if (!plan || !d_cells || !d_out) fail_validation("normalize: null argument");
+    if (photon_count < 1) fail_validation("normalize: photon_count must be >= 1");
+    ck(cudaSetDevice(plan->device), "cudaSetDevice");
+    const long long nvox = static_cast<long long>(plan->nx) * plan->ny * plan->nz;
+    const double q = vmc_quantum_for(plan->cfg.photon_count);
+    const double v = plan->voxel_mm * plan->voxel_mm * plan->voxel_mm;
+    const double scale = normalized ? q / (v * static_cast<double>(photon_count)) : q;
+    const long long n = sum_gates ? nvox : nvox * plan->cfg.ngates;
+    const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+    k_normalize<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const long long*>(d_cells), static_cast<const uint8_t*>(plan->labels.p),
+        static_cast<const double*>(plan->mua.p), nvox, plan->cfg.ngates, sum_gates, normalized, scale, d_out);
+    ck(cudaGetLastError(), "launch normalize");
+  });
+}
+
+uint64_t vmc_fnv1a64(const void* data, size_t bytes) {
+  const unsigned char* b = static_cast<const unsigned char*>(data);
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
 }
 
 int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags) {

@@ -447,6 +447,15 @@ class Plan:
         _check(lib().vmc_plan_trace(self._h, first, count, out.ctypes.data))
         return out
 
+    def normalize_torch(self, cells, out, photon_count: int, sum_gates: bool = True,
+                        normalized: bool = True, stream=None) -> None:
+        """K4 on the device: float32 fluence (or raw weight) from int64 cells."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(lib().vmc_plan_normalize(self._h, C.c_void_p(cells.data_ptr()), photon_count,
+                                        C.c_void_p(out.data_ptr()), 1 if sum_gates else 0,
+                                        1 if normalized else 0, C.c_void_p(st.cuda_stream)))
+
     def launches_per_run(self) -> int:
         return int(lib().vmc_plan_launches_per_run(self._h, 0))
 
