@@ -369,7 +369,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   // FP32 product path: K1 v2 (per-warp photon pool); VMC_KERNEL=v1 selects the
   // register-resident v1 kernel (kept for comparison). FP64 parity: v1<double>.
   const char* kv = std::getenv("VMC_KERNEL");
-  P->pool = !f64 && !(kv && std::strcmp(kv, "v1") == 0);
+  P->pool = !f64 && kv && std::strcmp(kv, "pool") == 0;
   if (P->pool) {
     A.box_cells = 0;
     A.scatter_pct = env_int("VMC_POOL_SCATTER_PCT", 100);

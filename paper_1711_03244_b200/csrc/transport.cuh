@@ -177,8 +177,10 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
 
   // photon state
   // 0 = ready to step, 1 = at a scattering point (scatter deferred to a scatter
-  // phase), 2 = no photon (lane waits for a refill)
+  // phase), 2 = no photon (lane waits for a refill), 3 = scatter in progress,
+  // waiting for another azimuth rejection-sampling try (ct/st kept in sct/sst)
   int phase = 2;
+  Real sct = 0, sst = 0;
   bool exhausted = false;  // warp-uniform: counter ran past `count`
   uint64_t idx = 0;
   Rng rng;
@@ -266,14 +268,16 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     phase = 2;
   };
 
+  unsigned dead = 0xffffffffu;  // lanes without a photon (warp-uniform view)
   for (;;) {
-    // ---- refill dead lanes: one atomicAdd per warp (dynamic claiming) ----
     // Warp-level phase scheduler. Photons are independent, so the order in
     // which a warp interleaves their events never changes any photon's
-    // arithmetic or RNG sequence; it only decides which lanes run together.
-    // A scatter is deferred until it can run with at least half of the
-    // working lanes; dead lanes are refilled in groups of kRefillMin.
-    unsigned dead = __ballot_sync(0xffffffffu, phase == 2);
+    // arithmetic or RNG sequence; it only decides which lanes run together:
+    //   step phase     every lane whose photon is ready to advance
+    //   scatter phase  lanes at a scattering point (phase 1) or waiting for an
+    //                  azimuth retry (phase 3); run once they are >= scatter_pct %
+    //                  of the live lanes, one rejection-sampling try per phase
+    //   refill         dead lanes (phase 2) relaunch in groups of refill_min
     if (!exhausted && dead && (__popc(dead) >= A.refill_min || dead == 0xffffffffu)) {
       const unsigned need = dead;
       {
@@ -381,6 +385,19 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       d_b = tb2;
       axis = 2;
     }
+    // neighbour across the nearest face; its label load is issued here so the
+    // L1/L2 latency overlaps the rest of the step (used only if the step crosses)
+    const Real dax = sel3(axis, dx, dy, dz);
+    const int stp = dax > Real(0) ? 1 : -1;
+    const int nvx = vx + (axis == 0 ? stp : 0);
+    const int nvy = vy + (axis == 1 ? stp : 0);
+    const int nvz = vz + (axis == 2 ? stp : 0);
+    const int stride = axis == 0 ? 1 : (axis == 1 ? nx : nxy32);
+    const int ncell = stp > 0 ? cell + stride : cell - stride;
+    const bool exterior = static_cast<unsigned>(nvx) >= static_cast<unsigned>(nx) ||
+                          static_cast<unsigned>(nvy) >= static_cast<unsigned>(ny) ||
+                          static_cast<unsigned>(nvz) >= static_cast<unsigned>(nz);
+    const int nlab_pf = static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
     Real d_s;
     if constexpr (kF32) {
       d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();
@@ -466,8 +483,6 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     } else {
       rs = fmax(0.0, rs - d * M.mus);
     }
-    const Real dax = sel3(axis, dx, dy, dz);
-    const int stp = dax > Real(0) ? 1 : -1;
     {
       // land exactly on the crossed plane; the other two coordinates advance
       const int vax = sel3(axis, vx, vy, vz);
@@ -476,13 +491,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       py = axis == 1 ? plane : py + dy * d;
       pz = axis == 2 ? plane : pz + dz * d;
     }
-    const int nvx = vx + (axis == 0 ? stp : 0);
-    const int nvy = vy + (axis == 1 ? stp : 0);
-    const int nvz = vz + (axis == 2 ? stp : 0);
-    const int stride = axis == 0 ? 1 : (axis == 1 ? nx : nxy32);
-    const int ncell = stp > 0 ? cell + stride : cell - stride;
-    const bool exterior = nvx < 0 || nvy < 0 || nvz < 0 || nvx >= nx || nvy >= ny || nvz >= nz;
-    const int nlab = exterior ? 0 : static_cast<int>(__ldg(A.labels + ncell));
+    const int nlab = exterior ? 0 : nlab_pf;
     const int c1 = M.nclass, c2 = sm_media[nlab].nclass;
     bool move = false, exited = false;
     if (!exterior && c1 == c2) {
@@ -609,14 +618,15 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     // ---- scatter phase: run the deferred scatters once at least half of the
     // lanes holding a photon are at a scattering point (or nobody can step) ----
     {
-      const unsigned pend = __ballot_sync(0xffffffffu, phase == 1);
-      const unsigned live = ~__ballot_sync(0xffffffffu, phase == 2);
+      const unsigned pend = __ballot_sync(0xffffffffu, (phase & 1) != 0);
+      dead = __ballot_sync(0xffffffffu, phase == 2);
+      const unsigned live = ~dead;
       if (pend != 0u && (pend == live || 100 * __popc(pend) >= A.scatter_pct * __popc(live))) {
-      if (phase == 1) {
+      if (phase & 1) {
           {
           // ---- scatter: hg_scatter (transport.cpp:126-147), new length ----
           const Medium<Real>& M = sm_media[lab];
-          phase = 0;
+          if (phase == 1) {
           if constexpr (kTrace || kDet) ++nscat;
           Real ct;
           {
@@ -641,23 +651,31 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           } else {
             st = sqrt(fmax(0.0, 1.0 - ct * ct));
           }
-          Real cp, sp;
-          for (;;) {  // sample_azimuth, transport.cpp:32-44
-            const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
-            const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
-            const Real r2 = ax_ * ax_ + ay_ * ay_;
-            if (r2 > Real(1e-12) && r2 <= Real(1)) {
-              Real k;
-              if constexpr (kF32) {
-                k = rsqrtf(r2);
-              } else {
-                k = 1.0 / sqrt(r2);
-              }
-              cp = ax_ * k;
-              sp = ay_ * k;
-              break;
-            }
+          sct = ct;
+          sst = st;
           }
+          // one try of the rejection azimuth (transport.cpp:32-44); a rejected
+          // lane keeps ct/st and retries in the next scatter phase, so the warp
+          // never loops on its unluckiest lane
+          Real cp, sp;
+          const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
+          const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
+          const Real r2 = ax_ * ax_ + ay_ * ay_;
+          if (!(r2 > Real(1e-12) && r2 <= Real(1))) {
+            phase = 3;
+          } else {
+          phase = 0;
+          {
+            Real k;
+            if constexpr (kF32) {
+              k = rsqrtf(r2);
+            } else {
+              k = 1.0 / sqrt(r2);
+            }
+            cp = ax_ * k;
+            sp = ay_ * k;
+          }
+          const Real ct = sct, st = sst;
           Real ox, oy, oz;
           if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
             ox = st * cp;
@@ -721,9 +739,11 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
             pd_kill += before - w;
             }
           }
+          }  // azimuth accepted
           }
 
       }
+      dead = __ballot_sync(0xffffffffu, phase == 2);  // roulette may have killed
       }
     }
   }

@@ -1,6 +1,6 @@
 """Per-region breakdown (warp-inst, thread-inst, simt) of the transport kernel
 from an ncu report. usage: sass_cats.py rep obj kernel N_photons  'name:lo-hi,...' """
-import collections, csv, io, subprocess, sys
+import collections, csv, io, os, subprocess, sys
 sys.path.insert(0, "tools")
 import sass_lines as S
 rep, obj, kern, n = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
@@ -15,7 +15,7 @@ for r in rows[2:]:
     (f, ln), _ = lm.get(int(r[0], 16) - base, ((None, 0), ""))
     name = "other"
     if f == "rng.cuh": name = "rng"
-    elif f == "transport.cuh":
+    elif f == os.environ.get("CATFILE", "transport.cuh"):
         for c, lo, hi in cats:
             if lo <= ln <= hi: name = c; break
     elif f and "atomic" in f: name = "atomics"
