@@ -51,7 +51,8 @@ def _compile(src: str, obj: str, extra, verbose: bool) -> None:
     if not _stale(objp, srcp):
         return
     if src.endswith(".cu"):
-        cmd = [NVCC] + ARCH + COMMON + extra + ["-c", srcp, "-o", objp]
+        tune = os.environ.get("VMC_NVCC_EXTRA", "").split() if obj == "transport_f32.o" else []
+        cmd = [NVCC] + ARCH + COMMON + extra + tune + ["-c", srcp, "-o", objp]
     else:  # host C++ (C++20 for the drop-in API), same visibility rules
         cmd = [CXX, "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall",
                "-I", os.path.join(ROOT, "include"), "-I", CSRC] + extra + ["-c", srcp, "-o", objp]

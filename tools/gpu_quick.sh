@@ -1,4 +1,7 @@
-python paper_1711_03244_b200/build.py >/dev/null
-echo "== v1"; VMC_KERNEL=v1 python tools/quick_tp.py 2>&1 | grep -E "tp"
-for pct in 35 50 70; do echo "pct=$pct"; VMC_KERNEL=v1 VMC_SCATTER_PCT=$pct python tools/quick_tp.py 2>&1 | grep -E "b1|b2"; done
+for v in "-DVMC_INCR_DDA=0 -DVMC_MIN_BLOCKS=5" "-DVMC_INCR_DDA=1 -DVMC_MIN_BLOCKS=4" "-DVMC_INCR_DDA=1 -DVMC_MIN_BLOCKS=5" "-DVMC_INCR_DDA=0 -DVMC_MIN_BLOCKS=4"; do
+  rm -f paper_1711_03244_b200/lib/obj/transport_f32.o
+  VMC_NVCC_EXTRA="$v" python paper_1711_03244_b200/build.py >/dev/null
+  echo "== $v"; python tools/quick_tp.py 2>&1 | grep -E "tp"
+done
+rm -f paper_1711_03244_b200/lib/obj/transport_f32.o; python paper_1711_03244_b200/build.py >/dev/null
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15

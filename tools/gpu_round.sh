@@ -1,13 +1,14 @@
-# usage: bash tools/gpu_round.sh <tag> [tests|notests] [ncu|noncu] [bench|nobench]
-TAG=${1:-dev}; T=${2:-tests}; N=${3:-ncu}; B=${4:-bench}
+# usage: bash tools/gpu_round.sh <tag>  — the per-change evidence run
+TAG=${1:-dev}
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 python paper_1711_03244_b200/build.py >/dev/null
-timeout 300 python tools/probe_gpu.py 2>&1 | tee gpurun_out/probe_$TAG.log | tail -8
-if [ "$T" = tests ]; then timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -25; fi
-if [ "$B" = bench ]; then timeout 400 python bench.py 2>&1 | tail -2 | tee gpurun_out/bench_$TAG.json; fi
-if [ "$N" = ncu ]; then
+timeout 300 python __graft_entry__.py smoke 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5
+timeout 400 python bench.py 2>&1 | tail -1 | tee gpurun_out/bench_$TAG.json
+timeout 400 python bench.py --impl reference --steps 2 --warmup 1 --cpu-seconds 6 2>&1 | tail -1 | tee gpurun_out/bench_ref_$TAG.json
+python tools/quick_tp.py 2>&1 | tee gpurun_out/tp_$TAG.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 --photons 10000000 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transport -s 1 -c 1 -o gpurun_out/prof_b2_$TAG python tools/ncu_target.py b2 1e7 > gpurun_out/ncu_full_$TAG.log 2>&1
-tail -2 gpurun_out/ncu_full_$TAG.log
+tail -1 gpurun_out/ncu_full_$TAG.log
 cp paper_1711_03244_b200/lib/obj/transport_f32.o gpurun_out/transport_f32_$TAG.o
-fi
