@@ -29,8 +29,6 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace);
 const void* transport_kernel_double(bool gates, bool det, bool trace);
-const void* transport_kernel_pool(bool gates, bool det, bool trace);
-int pool_smem_bytes(bool det, bool trace);
 }  // namespace vmc
 
 namespace {
@@ -242,7 +240,6 @@ struct vmc_plan {
   int sms = 0;
   int block = vmc::kBlock;
   size_t smem = 0, smem_trace = 0;
-  bool pool = false;
   int grid = 0, grid_trace = 0;
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
@@ -306,18 +303,14 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.iso_source = s->isotropic ? 1 : 0;
   A.media = P->media.p;
   for (int k = 0; k < 3; ++k) A.src_pos[k] = s->src_pos[k];
-  int center[3];
   if (!s->isotropic) {
     const HostLaunch L = pencil_launch(s);
     for (int k = 0; k < 3; ++k) {
       A.dir0[k] = L.dir[k];
       A.pos0[k] = L.pos[k];
       A.v0[k] = L.v[k];
-      center[k] = L.v[k] + static_cast<int>(std::lround(L.dir[k] * 7.0));
     }
     A.lab0 = s->labels[static_cast<size_t>(L.v[0]) + static_cast<size_t>(s->nx) * (L.v[1] + static_cast<size_t>(s->ny) * L.v[2])];
-  } else {
-    for (int k = 0; k < 3; ++k) center[k] = static_cast<int>(std::floor(s->src_pos[k] / s->voxel_mm));
   }
   A.seed = c->master_seed;
   A.tmax = c->tmax_ns;
@@ -331,31 +324,14 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.claim = static_cast<unsigned long long*>(P->claim.p);
   A.error_flag = static_cast<int*>(P->err.p);
 
-  // hot box: up to 16^3 cells per gate within a 32 KB (lo/hi u32) budget,
-  // placed around the launch voxel and pushed along the launch direction.
-  {
-    const int dims[3] = {s->nx, s->ny, s->nz};
-    int side = 16;
-    while (side > 1 && static_cast<long long>(side) * side * side * c->ngates * 8 > 32 * 1024) --side;
-    int n[3], o[3];
-    for (int k = 0; k < 3; ++k) {
-      n[k] = std::min(side, dims[k]);
-      o[k] = center[k] - n[k] / 2;
-      o[k] = std::max(0, std::min(o[k], dims[k] - n[k]));
-    }
-    A.bx0 = o[0];
-    A.by0 = o[1];
-    A.bz0 = o[2];
-    A.bnx = n[0];
-    A.bny = n[1];
-    A.bnz = n[2];
-    A.box_cells = side >= 4 ? n[0] * n[1] * n[2] * c->ngates : 0;
-    // Measured on B200: L2 atomics absorb the source hot spot (<= 2e8 adds/s on one
-    // cell) and the box's extra address math costs more than it saves, so it is
-    // off unless VMC_HOTBOX=1.
-    const char* env = std::getenv("VMC_HOTBOX");
-    if (!(env && env[0] == '1')) A.box_cells = 0;
-  }
+  A.hf = static_cast<float>(A.h);
+  A.inv_hf = static_cast<float>(1.0 / A.h);
+  A.tmaxf = static_cast<float>(A.tmax);
+  A.rthrf = static_cast<float>(A.rthr);
+  A.rmultf = static_cast<float>(A.rmult);
+  A.inv_rmultf = static_cast<float>(A.inv_rmult);
+  A.inv_gate_wf = static_cast<float>(A.inv_gate_w);
+  A.qscalef = static_cast<float>(A.qscale);
   A.scatter_pct = env_int("VMC_SCATTER_PCT", 50);
   A.refill_min = env_int("VMC_REFILL_MIN", 2);
   A.ndet = c->ndet;
@@ -366,25 +342,10 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.det_cap = c->det_capacity;
 
   const bool gates = c->ngates > 1, det = c->ndet > 0;
-  // FP32 product path: K1 v2 (per-warp photon pool); VMC_KERNEL=v1 selects the
-  // register-resident v1 kernel (kept for comparison). FP64 parity: v1<double>.
-  const char* kv = std::getenv("VMC_KERNEL");
-  P->pool = !f64 && kv && std::strcmp(kv, "pool") == 0;
-  if (P->pool) {
-    A.box_cells = 0;
-    A.scatter_pct = env_int("VMC_POOL_SCATTER_PCT", 100);
-    A.refill_min = env_int("VMC_POOL_REFILL_MIN", 8);
-    P->kern = vmc::transport_kernel_pool(gates, det, false);
-    P->kern_trace = vmc::transport_kernel_pool(gates, det, true);
-    const size_t mb = (media_bytes + 15) & ~static_cast<size_t>(15);
-    P->smem = mb + static_cast<size_t>(vmc::pool_smem_bytes(det, false));
-    P->smem_trace = mb + static_cast<size_t>(vmc::pool_smem_bytes(det, true));
-  } else {
-    P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
-    P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
-    P->smem = media_bytes + static_cast<size_t>(A.box_cells) * 8;
-    P->smem_trace = P->smem;
-  }
+  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
+  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
+  P->smem = media_bytes;
+  P->smem_trace = media_bytes;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem_trace)),
@@ -421,13 +382,6 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   A.trace = d_trace;
   void* argv[] = {&A};
   // never launch more persistent threads than photons need
-  if (P->pool && count > 0xffffffffull) {
-    // the pool keeps the photon offset in 32 bits: split very large ranges
-    for (uint64_t off = 0; off < count; off += 0x80000000ull)
-      plan_enqueue(P, first + off, std::min<uint64_t>(0x80000000ull, count - off), d_cells, d_totals, d_det,
-                   d_det_count, st, 0u, trace, d_trace ? d_trace + off : nullptr);
-    return;
-  }
   const uint64_t need_blocks = (count + P->block - 1) / P->block;
   const int full = trace ? P->grid_trace : P->grid;
   const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));

@@ -75,8 +75,8 @@ struct KernelArgs {
   double qscale;  // 1 / quantum
   long long* cells;
   long long* totals;  // [4] deposited, escaped, killed, truncated quanta
-  // shared-memory hot box (cells of all gates), disabled when box_cells == 0
-  int bx0, by0, bz0, bnx, bny, bnz, box_cells, pad2;
+  // float copies of the hot constants (no FP64 conversion inside the loop)
+  float hf, tmaxf, rthrf, rmultf, inv_rmultf, inv_gate_wf, qscalef, inv_hf;
   // detectors
   int ndet, nppath, rec_stride, pad3;
   // warp scheduling: scatter phase when >= scatter_pct % of live lanes wait;
@@ -110,12 +110,32 @@ struct RealTraits<float> {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
   }
+  static __device__ __forceinline__ float rsqrt(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
+  // natural log via MUFU.LG2 (argument is a normal float here)
+  static __device__ __forceinline__ float ln(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * 0.69314718055994531f;
+  }
+  // exp(-x), x >= 0, via MUFU.EX2
+  static __device__ __forceinline__ float exp_neg(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x * -1.4426950408889634f));
+    return r;
+  }
 };
 template <>
 struct RealTraits<double> {
   static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
   static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
   static __device__ __forceinline__ double sqrt_(double x) { return sqrt(x); }
+  static __device__ __forceinline__ double rsqrt(double x) { return 1.0 / sqrt(x); }
+  static __device__ __forceinline__ double ln(double x) { return log(x); }
+  static __device__ __forceinline__ double exp_neg(double x) { return exp(-x); }
 };
 
 // pick component `axis` of (x, y, z) without dynamic register indexing
@@ -147,28 +167,25 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   constexpr bool kF32 = std::is_same<Real, float>::value;
   using Rng = Xs128p<kTrace>;
 
-  // ---- shared memory: media table, per-CTA hot box (lo/hi words) ---------
+  // ---- shared memory: media table ---------------------------------------
   Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem);
-  unsigned int* box_lo = reinterpret_cast<unsigned int*>(smem + sizeof(Medium<Real>) * A.nmedia);
-  unsigned int* box_hi = box_lo + A.box_cells;
   {
     const Medium<Real>* gm = static_cast<const Medium<Real>*>(A.media);
     const int nwords = static_cast<int>(sizeof(Medium<Real>) / 4) * A.nmedia;
     for (int i = threadIdx.x; i < nwords; i += blockDim.x)
       reinterpret_cast<int*>(sm_media)[i] = reinterpret_cast<const int*>(gm)[i];
-    for (int i = threadIdx.x; i < 2 * A.box_cells; i += blockDim.x) box_lo[i] = 0u;
   }
   __syncthreads();
 
   const int nx = A.nx, ny = A.ny, nz = A.nz;
   const int nxy32 = static_cast<int>(A.nxy);
-  const Real h = static_cast<Real>(A.h);
-  const Real tmax = static_cast<Real>(A.tmax);
-  const Real rthr = static_cast<Real>(A.rthr);
-  const Real rmult = static_cast<Real>(A.rmult);
-  const Real inv_rmult = static_cast<Real>(A.inv_rmult);
-  const Real inv_gate_w = static_cast<Real>(A.inv_gate_w);
-  const float qscale_f = static_cast<float>(A.qscale);
+  const Real h = kF32 ? Real(A.hf) : Real(A.h);
+  const Real tmax = kF32 ? Real(A.tmaxf) : Real(A.tmax);
+  const Real rthr = kF32 ? Real(A.rthrf) : Real(A.rthr);
+  const Real rmult = kF32 ? Real(A.rmultf) : Real(A.rmult);
+  const Real inv_rmult = kF32 ? Real(A.inv_rmultf) : Real(A.inv_rmult);
+  const Real inv_gate_w = kF32 ? Real(A.inv_gate_wf) : Real(A.inv_gate_w);
+  const float qscale_f = A.qscalef;
   const int lane = threadIdx.x & 31;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -198,20 +215,11 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
 #pragma unroll
   for (int m = 0; m < (kDet ? kMaxDetMedia : 1); ++m) ppath[m] = 0;
 
-  auto deposit = [&](int c, int gt, int bvx, int bvy, int bvz, long long q) {
-    if (q == 0) return;
-    if (A.box_cells) {
-      const unsigned ux = static_cast<unsigned>(bvx - A.bx0), uy = static_cast<unsigned>(bvy - A.by0),
-                     uz = static_cast<unsigned>(bvz - A.bz0);
-      if (ux < static_cast<unsigned>(A.bnx) && uy < static_cast<unsigned>(A.bny) &&
-          uz < static_cast<unsigned>(A.bnz)) {
-        const int bi = static_cast<int>(ux + A.bnx * (uy + A.bny * (uz + A.bnz * gt)));
-        smem_add_u64(box_lo + bi, box_hi + bi, static_cast<unsigned long long>(q));
-        return;
-      }
-    }
-    atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt),
-              static_cast<unsigned long long>(q));
+  // one fixed-point add per deposit run (red.global.add.u64; the map is L2-resident)
+  auto deposit = [&](int c, int gt, int, int, int, long long q) {
+    if (q != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt),
+                static_cast<unsigned long long>(q));
   };
   auto quant = [&](Real x) -> long long {
     if constexpr (kF32) {
@@ -240,7 +248,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     const Real u = rng.template unit<Real>();
     if constexpr (kF32) {
       // u == 0 (p = 2^-24) stands for the reference's [0, 2^-24) cell: use 2^-25.
-      return -__logf(u > 0.0f ? u : 0x1p-25f);  // MUFU.LG2: abs. error ~1e-7
+      return -Tr::ln(u > 0.0f ? u : 0x1p-25f);  // MUFU.LG2: abs. error ~1e-7
     } else {
       return -log(u > 0.0 ? u : 4.9406564584124654e-324);
     }
@@ -375,28 +383,33 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       tb1 = dy != Real(0) ? (t1_ > Real(0) ? t1_ : Real(0)) : Tr::inf();
       tb2 = dz != Real(0) ? (t2_ > Real(0) ? t2_ : Real(0)) : Tr::inf();
     }
+    // select-style argmin (ties -> lower axis), carrying the crossed axis'
+    // direction component, voxel coordinate, extent and cell stride along
     int axis = 0;
-    Real d_b = tb0;
+    Real d_b = tb0, dax = dx;
+    int vax = vx, nax = nx, stride = 1;
     if (tb1 < d_b) {
       d_b = tb1;
       axis = 1;
+      dax = dy;
+      vax = vy;
+      nax = ny;
+      stride = nx;
     }
     if (tb2 < d_b) {
       d_b = tb2;
       axis = 2;
+      dax = dz;
+      vax = vz;
+      nax = nz;
+      stride = nxy32;
     }
     // neighbour across the nearest face; its label load is issued here so the
     // L1/L2 latency overlaps the rest of the step (used only if the step crosses)
-    const Real dax = sel3(axis, dx, dy, dz);
     const int stp = dax > Real(0) ? 1 : -1;
-    const int nvx = vx + (axis == 0 ? stp : 0);
-    const int nvy = vy + (axis == 1 ? stp : 0);
-    const int nvz = vz + (axis == 2 ? stp : 0);
-    const int stride = axis == 0 ? 1 : (axis == 1 ? nx : nxy32);
+    const int nvax = vax + stp;
     const int ncell = stp > 0 ? cell + stride : cell - stride;
-    const bool exterior = static_cast<unsigned>(nvx) >= static_cast<unsigned>(nx) ||
-                          static_cast<unsigned>(nvy) >= static_cast<unsigned>(ny) ||
-                          static_cast<unsigned>(nvz) >= static_cast<unsigned>(nz);
+    const bool exterior = static_cast<unsigned>(nvax) >= static_cast<unsigned>(nax);
     const int nlab_pf = static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
     Real d_s;
     if constexpr (kF32) {
@@ -422,7 +435,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       Real e;
       const Real taylor = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
       if constexpr (kF32) {
-        e = x < 0.01f ? taylor : __expf(-x);  // branch-free select
+        e = x < 0.01f ? taylor : Tr::exp_neg(x);  // branch-free select
       } else {
         e = x < 0.01 ? taylor : exp(-x);
       }
@@ -485,7 +498,6 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     }
     {
       // land exactly on the crossed plane; the other two coordinates advance
-      const int vax = sel3(axis, vx, vy, vz);
       const Real plane = static_cast<Real>(vax + (stp > 0 ? 1 : 0)) * h;
       px = axis == 0 ? plane : px + dx * d;
       py = axis == 1 ? plane : py + dy * d;
@@ -529,7 +541,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           Real qz = axis == 2 ? (dax > Real(0) ? cost : -cost) : dz * eta;
           Real k;
           if constexpr (kF32) {
-            k = rsqrtf(qx * qx + qy * qy + qz * qz);
+            k = Tr::rsqrt(qx * qx + qy * qy + qz * qz);
           } else {
             k = 1.0 / sqrt(qx * qx + qy * qy + qz * qz);
           }
@@ -599,9 +611,9 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         run_w0 = w;
         gate = ng;
       }
-      vx = nvx;
-      vy = nvy;
-      vz = nvz;
+      vx += axis == 0 ? stp : 0;
+      vy += axis == 1 ? stp : 0;
+      vz += axis == 2 ? stp : 0;
       cell = ncell;
       lab = nlab;
     } else if constexpr (kGates && kF32) {
@@ -668,7 +680,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           {
             Real k;
             if constexpr (kF32) {
-              k = rsqrtf(r2);
+              k = Tr::rsqrt(r2);
             } else {
               k = 1.0 / sqrt(r2);
             }
@@ -684,7 +696,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           } else {
             if constexpr (kF32) {
               const float one_m = 1.0f - dz * dz;
-              const float rden = rsqrtf(one_m);
+              const float rden = Tr::rsqrt(one_m);
               const float den = one_m * rden;
               const float sr = st * rden;
               ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
@@ -701,7 +713,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
             const Real n2 = ox * ox + oy * oy + oz * oz;
             if constexpr (kF32) {
               if (fabsf(n2 - 1.0f) > 1e-6f) {
-                const float k = rsqrtf(n2);
+                const float k = Tr::rsqrt(n2);
                 ox *= k;
                 oy *= k;
                 oz *= k;
@@ -763,24 +775,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     if (acc_kill) atomicAdd(tot + 2, static_cast<unsigned long long>(acc_kill));
     if (acc_trunc) atomicAdd(tot + 3, static_cast<unsigned long long>(acc_trunc));
   }
-  if (A.box_cells) {
-    __syncthreads();
-    const int per_gate = A.bnx * A.bny * A.bnz;
-    for (int i = threadIdx.x; i < A.box_cells; i += blockDim.x) {
-      const unsigned long long v =
-          (static_cast<unsigned long long>(box_hi[i]) << 32) | static_cast<unsigned long long>(box_lo[i]);
-      if (v) {
-        const int gt = i / per_gate;
-        int r = i - gt * per_gate;
-        const int bx = r % A.bnx;
-        r /= A.bnx;
-        const int by = r % A.bny;
-        const int bz = r / A.bny;
-        const long long c = (A.bx0 + bx) + nx * ((A.by0 + by) + static_cast<long long>(ny) * (A.bz0 + bz));
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt), v);
-      }
-    }
-  }
+
 }
 
 }  // namespace vmc

@@ -3,7 +3,6 @@
 // the product path) and once with -DVMC_REAL=double --fmad=false (parity mode;
 // no contraction, like the reference built with -ffp-contract=off).
 #include "transport.cuh"
-#include "transport_pool.cuh"
 
 #ifndef VMC_REAL
 #define VMC_REAL float
@@ -46,32 +45,5 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
   }
 }
 
-#if VMC_REAL_IS_FLOAT
-template <bool G, bool D, bool T>
-__global__ void __launch_bounds__(kBlock, 4) k_transport_pool(const __grid_constant__ KernelArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  pool_body<G, D, T>(A, smem);
-}
-
-// K1 v2 (per-warp photon pool), FP32 only.
-const void* transport_kernel_pool(bool gates, bool det, bool trace) {
-  const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
-  switch (key) {
-    case 0: return reinterpret_cast<const void*>(&k_transport_pool<false, false, false>);
-    case 1: return reinterpret_cast<const void*>(&k_transport_pool<false, false, true>);
-    case 2: return reinterpret_cast<const void*>(&k_transport_pool<false, true, false>);
-    case 3: return reinterpret_cast<const void*>(&k_transport_pool<false, true, true>);
-    case 4: return reinterpret_cast<const void*>(&k_transport_pool<true, false, false>);
-    case 5: return reinterpret_cast<const void*>(&k_transport_pool<true, false, true>);
-    case 6: return reinterpret_cast<const void*>(&k_transport_pool<true, true, false>);
-    default: return reinterpret_cast<const void*>(&k_transport_pool<true, true, true>);
-  }
-}
-int pool_smem_bytes(bool det, bool trace) {
-  const int per_warp = det ? (trace ? pool_smem_per_warp<true, true>() : pool_smem_per_warp<true, false>())
-                           : (trace ? pool_smem_per_warp<false, true>() : pool_smem_per_warp<false, false>());
-  return per_warp * (kBlock / 32);
-}
-#endif
 
 }  // namespace vmc
