@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N>1 (gloo only for plumbing tests)")
     return ap.parse_args()
 
 
@@ -158,12 +160,11 @@ def run_reference(args, rank: int, world: int):
 
 # ---------------------------------------------------------------------------
 def run_b200(args, rank: int, world: int, local_rank: int):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1711_03244_b200 as v
-    from paper_1711_03244_b200 import _abi
+    from paper_1711_03244_b200.distributed import rank_ranges, reduce_to_root
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -172,9 +173,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     st = v.baseline_setup(args.workload, photons=total, seed=args.seed)
     cfg = st.config
     # contiguous range of this rank (partition_s1 over identical GPUs)
-    counts = v.make_partition(total, [v.DeviceProfile(cores=1, gpu=i) for i in range(world)], v.Strategy.S1).counts
-    first = sum(counts[:rank])
-    mine = counts[rank]
+    first, mine = rank_ranges(total, world)[rank]
 
     plan = v.Plan(st.scene, cfg, local_rank)
     cells = torch.zeros(plan.ncells, dtype=torch.int64, device=dev)
@@ -192,9 +191,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         plan.run_torch(first, mine, cells, totals, det, det_n, stream=stream, zero=True)
         if k_ev is not None:
             k_ev[1].record(stream)
-        if world > 1:
-            dist.reduce(cells, dst=0, op=dist.ReduceOp.SUM)
-            dist.reduce(totals, dst=0, op=dist.ReduceOp.SUM)
+        if world > 1:  # the one exchange step: int64 map + dispositions onto rank 0
+            reduce_to_root(cells, totals)
 
     for _ in range(args.warmup):
         step()
@@ -304,6 +302,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.backend == "gloo":
+        # plumbing test mode: ranks may share a GPU
+        import torch
+        local_rank %= max(1, torch.cuda.device_count())
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -312,7 +314,10 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     try:
         run_b200(args, rank, world, local_rank)
     finally:

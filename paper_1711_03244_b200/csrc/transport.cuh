@@ -38,6 +38,10 @@
 
 namespace vmc {
 
+#ifndef VMC_SUBSTEPS
+#define VMC_SUBSTEPS 1
+#endif
+constexpr int kSubSteps = VMC_SUBSTEPS;  // steps per warp iteration before the scatter check
 constexpr int kBlock = 256;  // threads per CTA of K1
 constexpr int kMaxDet = 16;
 constexpr int kMaxDetMedia = 8;
@@ -367,7 +371,11 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       if (exhausted) break;
       continue;
     }
-    do {  // ---- step phase: every lane holding a photon that is not at a scattering point
+    // ---- step phase(s): every lane holding a photon that is not at a
+    // scattering point advances by up to kSubSteps steps before the scatter check
+#pragma unroll 1
+    for (int sub = 0; sub < kSubSteps; ++sub) {
+    do {
     if (phase != 0) break;
     // ---- one advance() step, transport.cpp:161-225 ----
     const Medium<Real>& M = sm_media[lab];
@@ -627,6 +635,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       }
     }
     } while (0);
+    }
     // ---- scatter phase: run the deferred scatters once at least half of the
     // lanes holding a photon are at a scattering point (or nobody can step) ----
     {

@@ -31,11 +31,17 @@ def rank_ranges(total: int, world: int, strategy: Strategy = Strategy.S1,
 
 
 def reduce_to_root(cells, totals, dst: int = 0) -> None:
-    """Sum int64 maps and disposition quanta onto `dst` (in place)."""
+    """Sum int64 maps and disposition quanta onto `dst` (in place). NCCL: one
+    reduce each (NVLink); gloo with CUDA tensors (plumbing tests, ranks sharing
+    a GPU) has no device reduce, so it all-reduces instead."""
     import torch.distributed as dist
     if dist.is_initialized() and dist.get_world_size() > 1:
-        dist.reduce(cells, dst=dst, op=dist.ReduceOp.SUM)
-        dist.reduce(totals, dst=dst, op=dist.ReduceOp.SUM)
+        if dist.get_backend() == "gloo" and cells.is_cuda:
+            dist.all_reduce(cells, op=dist.ReduceOp.SUM)
+            dist.all_reduce(totals, op=dist.ReduceOp.SUM)
+        else:
+            dist.reduce(cells, dst=dst, op=dist.ReduceOp.SUM)
+            dist.reduce(totals, dst=dst, op=dist.ReduceOp.SUM)
 
 
 def run_sharded(total: int, compute: Callable[[int, int], tuple], rank: int, world: int,

@@ -1,7 +1,6 @@
-for v in "-DVMC_INCR_DDA=0 -DVMC_MIN_BLOCKS=5" "-DVMC_INCR_DDA=1 -DVMC_MIN_BLOCKS=4" "-DVMC_INCR_DDA=1 -DVMC_MIN_BLOCKS=5" "-DVMC_INCR_DDA=0 -DVMC_MIN_BLOCKS=4"; do
+for v in "-DVMC_SUBSTEPS=1" "-DVMC_SUBSTEPS=2" "-DVMC_SUBSTEPS=3"; do
   rm -f paper_1711_03244_b200/lib/obj/transport_f32.o
   VMC_NVCC_EXTRA="$v" python paper_1711_03244_b200/build.py >/dev/null
   echo "== $v"; python tools/quick_tp.py 2>&1 | grep -E "tp"
 done
 rm -f paper_1711_03244_b200/lib/obj/transport_f32.o; python paper_1711_03244_b200/build.py >/dev/null
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15
