@@ -52,7 +52,6 @@ def test_bench_two_ranks_gloo(gpu):
     assert line["n_gpus"] == 2 and line["config"]["photons_total"] == 1_000_000
 
 
-@pytest.mark.gpu
 def test_bench_reference_arm():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
                         "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=300)
