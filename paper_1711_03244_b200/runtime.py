@@ -192,20 +192,28 @@ def _det_buffer(m: Marshalled, config: SimulationConfig):
 
 
 def run_group_dynamic(first_index: int, quota: int, threads: int, scene: Scene,
-                      config: SimulationConfig, device: int = 0) -> GroupRunResult:
+                      config: SimulationConfig, device: int = 0, cells_out: Optional[np.ndarray] = None,
+                      det_out: Optional[np.ndarray] = None) -> GroupRunResult:
     """Photons [first_index, first_index+quota) on one B200 (scheduler.cpp:321-324).
 
     `threads` is validated as in the reference (>= 1); the device runs its
     own persistent worker grid, so the whole quota is reported in slot 0 of
-    per_thread_photons (Σ == quota, size == threads)."""
+    per_thread_photons (Σ == quota, size == threads). `cells_out` / `det_out`
+    may be preallocated (e.g. pinned) host buffers that are overwritten."""
     if threads < 1:
         raise ValidationError("run_group: threads must be >= 1")
     config.validate()
     m = Marshalled(scene, config)
     nx, ny, nz = scene.grid.dims
-    cells = np.zeros((config.ngates, nz, ny, nx), np.int64)
+    shape = (config.ngates, nz, ny, nx)
+    if cells_out is not None:
+        if cells_out.dtype != np.int64 or cells_out.size != m.ncells or not cells_out.flags.c_contiguous:
+            raise ValidationError("cells_out must be a contiguous int64 array of ngates*nx*ny*nz cells")
+        cells = cells_out.reshape(shape)
+    else:
+        cells = np.zeros(shape, np.int64)
     tot = _abi.vmc_disposition()
-    det = _det_buffer(m, config)
+    det = _det_buffer(m, config) if det_out is None else det_out
     ndet = C.c_uint64(0)
     wall = C.c_double(0.0)
     _check(lib().vmc_run_range(C.byref(m.scene), C.byref(m.config), first_index, quota, device,
