@@ -171,8 +171,21 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   constexpr bool kF32 = std::is_same<Real, float>::value;
   using Rng = Xs128p<kTrace>;
 
-  // ---- shared memory: media table ---------------------------------------
+  // ---- shared memory: media table, then per-thread "cold" state (values
+  // touched only at photon end / azimuth retries / records), structure of
+  // arrays so each access is bank-conflict free; keeps the loop under 64 regs
   Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem);
+  unsigned char* cold = smem + ((sizeof(Medium<Real>) * A.nmedia + 15) & ~static_cast<size_t>(15));
+  const int tid = threadIdx.x;
+  long long* c_esc = reinterpret_cast<long long*>(cold) + tid;
+  long long* c_kill = c_esc + kBlock;
+  long long* c_trunc = c_kill + kBlock;
+  uint64_t* c_idx = reinterpret_cast<uint64_t*>(c_trunc + kBlock);
+  Real* c_sct = reinterpret_cast<Real*>(reinterpret_cast<uint64_t*>(cold) + 4 * kBlock) + tid;
+  Real* c_sst = c_sct + kBlock;
+  *c_esc = 0;
+  *c_kill = 0;
+  *c_trunc = 0;
   {
     const Medium<Real>* gm = static_cast<const Medium<Real>*>(A.media);
     const int nwords = static_cast<int>(sizeof(Medium<Real>) / 4) * A.nmedia;
@@ -194,16 +207,14 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
   // per-thread fixed-point disposition totals
-  long long acc_dep = 0, acc_esc = 0, acc_kill = 0, acc_trunc = 0;
+  long long acc_dep = 0;  // escaped/killed/truncated quanta live in shared memory (c_*)
 
   // photon state
   // 0 = ready to step, 1 = at a scattering point (scatter deferred to a scatter
   // phase), 2 = no photon (lane waits for a refill), 3 = scatter in progress,
   // waiting for another azimuth rejection-sampling try (ct/st kept in sct/sst)
   int phase = 2;
-  Real sct = 0, sst = 0;
   bool exhausted = false;  // warp-uniform: counter ran past `count`
-  uint64_t idx = 0;
   Rng rng;
   rng.a = rng.b = 0;
   Real px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, ix = 0, iy = 0, iz = 0;
@@ -269,13 +280,13 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
       tr.escaped = pd_esc;
       tr.killed = pd_kill;
       tr.truncated = pd_trunc;
-      A.trace[idx - A.first] = tr;
+      A.trace[*c_idx - A.first] = tr;
     }
     if constexpr (!kF32) {
       acc_dep += llround(pd_dep * A.qscale);
-      acc_esc += llround(pd_esc * A.qscale);
-      acc_kill += llround(pd_kill * A.qscale);
-      acc_trunc += llround(pd_trunc * A.qscale);
+      *c_esc += llround(pd_esc * A.qscale);
+      *c_kill += llround(pd_kill * A.qscale);
+      *c_trunc += llround(pd_trunc * A.qscale);
     }
     phase = 2;
   };
@@ -301,7 +312,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           const unsigned long long my = base + __popc(need & lanemask_lt);
           if (my < A.count) {
             // ---- launch, transport.cpp:83-106 ----
-            idx = A.first + my;
+            const uint64_t idx = A.first + my;
+            *c_idx = idx;
             rng.seed(A.seed, idx);
             Real ux, uy, uz;
             if (A.iso_source) {
@@ -473,7 +485,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         const long long q = quant(run_w0 - w);
         deposit(cell, gate, vx, vy, vz, q);
         acc_dep += q;
-        acc_trunc += quant(w);
+        *c_trunc += quant(w);
       }
       pd_trunc += w;
       finish(2);
@@ -565,7 +577,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
         const long long q = quant(run_w0 - w);
         deposit(cell, gate, vx, vy, vz, q);
         acc_dep += q;
-        acc_esc += quant(w);
+        *c_esc += quant(w);
       }
       pd_esc += w;
       if constexpr (kDet) {
@@ -592,7 +604,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
             if (slot < A.det_cap) {
               unsigned char* rec = A.det_out + slot * static_cast<unsigned long long>(A.rec_stride);
               vmc_det_record_head hd;
-              hd.photon_index = idx;
+              hd.photon_index = *c_idx;
               hd.det_id = static_cast<uint32_t>(hit);
               hd.nscat = nscat;
               hd.w_exit = static_cast<float>(w);
@@ -672,8 +684,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
           } else {
             st = sqrt(fmax(0.0, 1.0 - ct * ct));
           }
-          sct = ct;
-          sst = st;
+          *c_sct = ct;
+          *c_sst = st;
           }
           // one try of the rejection azimuth (transport.cpp:32-44); a rejected
           // lane keeps ct/st and retries in the next scatter phase, so the warp
@@ -696,7 +708,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
             cp = ax_ * k;
             sp = ay_ * k;
           }
-          const Real ct = sct, st = sst;
+          const Real ct = *c_sct, st = *c_sst;
           Real ox, oy, oz;
           if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
             ox = st * cp;
@@ -748,13 +760,13 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
               acc_dep += q;
             }
             if (!survive) {
-              if constexpr (kF32) acc_kill += quant(before);
+              if constexpr (kF32) *c_kill += quant(before);
               pd_kill += before;
               finish(1);
             } else {
             w *= rmult;
             if constexpr (kF32) {
-              acc_kill += quant(before) - quant(w);
+              *c_kill += quant(before) - quant(w);
               run_w0 = w;
             }
             pd_kill += before - w;
@@ -769,7 +781,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned cha
     }
   }
 
-  // ---- epilogue: dispositions (warp reduce), hot-box flush -------------
+  // ---- epilogue: dispositions (warp reduce) -------------------------------
+  long long acc_esc = *c_esc, acc_kill = *c_kill, acc_trunc = *c_trunc;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     acc_dep += __shfl_xor_sync(0xffffffffu, acc_dep, o);

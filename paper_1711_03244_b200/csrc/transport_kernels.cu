@@ -10,17 +10,24 @@
 
 namespace vmc {
 
-// FP32: cap registers at 64 so 4 CTAs (32 warps) stay resident per SM;
-// measured faster than the unconstrained allocation (fewer warps).
+// Occupancy: the plain FP32 kernel fits 48 registers without spills -> 5 CTAs
+// (40 warps) per SM; the gated / detector / trace variants carry more state and
+// are capped at 64 registers (4 CTAs). FP64 (parity mode) is unconstrained.
 #ifndef VMC_MIN_BLOCKS
 #if VMC_REAL_IS_FLOAT
-#define VMC_MIN_BLOCKS 4
+#define VMC_MIN_BLOCKS_PLAIN 5
+#define VMC_MIN_BLOCKS_RICH 4
 #else
-#define VMC_MIN_BLOCKS 1
+#define VMC_MIN_BLOCKS_PLAIN 1
+#define VMC_MIN_BLOCKS_RICH 1
 #endif
+#else
+#define VMC_MIN_BLOCKS_PLAIN VMC_MIN_BLOCKS
+#define VMC_MIN_BLOCKS_RICH VMC_MIN_BLOCKS
 #endif
 template <typename Real, bool G, bool D, bool T>
-__global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS) k_transport(const __grid_constant__ KernelArgs A) {
+__global__ void __launch_bounds__(kBlock, (G || D || T) ? VMC_MIN_BLOCKS_RICH : VMC_MIN_BLOCKS_PLAIN)
+    k_transport(const __grid_constant__ KernelArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   transport_body<Real, G, D, T>(A, smem);
 }
