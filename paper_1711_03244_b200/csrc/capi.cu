@@ -546,6 +546,20 @@ __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* 
   }
 }
 
+// K3 fallback: dst += src over int64 cells (exact integer sum, order-free).
+__global__ void k_add_i64(long long* __restrict__ dst, const long long* __restrict__ src, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+void add_i64(int64_t* dst, const int64_t* src, uint64_t n, cudaStream_t st) {
+  const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, 148ull * 8));
+  k_add_i64<<<std::max(grid, 1), 256, 0, st>>>(reinterpret_cast<long long*>(dst),
+                                               reinterpret_cast<const long long*>(src), static_cast<long long>(n));
+  ck(cudaGetLastError(), "launch add_i64");
+}
+
 __global__ void k_rng_kat(uint64_t seed, uint64_t stream, int n, uint64_t* out) {
   vmc::Xs128p<false> r;
   r.seed(seed, stream);
@@ -683,7 +697,40 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
     const uint64_t ncells = slot[0].plan->ncells;
     double red_ms = 0.0;
     try {
-      if (ndev > 1) {
+      bool distinct = true;
+      for (int i = 0; i < ndev; ++i)
+        for (int j = 0; j < i; ++j) distinct &= devices[i] != devices[j];
+      const char* mode = std::getenv("VMC_MULTI_REDUCE");
+      const bool want_peer = !distinct || (mode && std::strcmp(mode, "peer") == 0);
+      if (ndev > 1 && want_peer) {
+        // device-side reduce without NCCL (repeated devices, or forced): peer copy
+        // of each partial map into a scratch buffer on devices[0] + an int64 add
+        // kernel there. Same integer sums as the NCCL path.
+        cudaSetDevice(devices[0]);
+        DevBuf scratch;
+        scratch.alloc((ncells + 4) * sizeof(int64_t), devices[0]);
+        cudaEvent_t r0, r1;
+        ck(cudaEventCreate(&r0), "event");
+        ck(cudaEventCreate(&r1), "event");
+        ck(cudaEventRecord(r0, slot[0].st), "event");
+        for (int i = 1; i < ndev; ++i) {
+          int64_t* sc = static_cast<int64_t*>(scratch.p);
+          ck(cudaMemcpyPeerAsync(sc, devices[0], slot[i].cells.p, devices[i], ncells * sizeof(int64_t), slot[0].st),
+             "peer copy");
+          ck(cudaMemcpyPeerAsync(sc + ncells, devices[0], slot[i].totals.p, devices[i], 4 * sizeof(int64_t),
+                                 slot[0].st),
+             "peer copy");
+          add_i64(static_cast<int64_t*>(slot[0].cells.p), sc, ncells, slot[0].st);
+          add_i64(static_cast<int64_t*>(slot[0].totals.p), sc + ncells, 4, slot[0].st);
+        }
+        ck(cudaEventRecord(r1, slot[0].st), "event");
+        ck(cudaStreamSynchronize(slot[0].st), "reduce");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r0, r1);
+        red_ms = ms;
+        cudaEventDestroy(r0);
+        cudaEventDestroy(r1);
+      } else if (ndev > 1) {
         // one exchange step: NCCL reduce of the int64 maps + totals onto devices[0]
         Nccl& N = nccl();
         std::vector<void*> comms(ndev, nullptr);

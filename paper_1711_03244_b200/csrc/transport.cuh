@@ -165,8 +165,13 @@ struct Walk;
 // ---------------------------------------------------------------------------
 // The kernel body (shared by both precisions).
 
+// Dynamic shared memory of K1, referenced through the symbol (not a generic
+// pointer) so every access compiles to LDS/STS with a constant window base.
+extern __shared__ __align__(16) unsigned char vmc_smem[];
+
 template <typename Real, bool kGates, bool kDet, bool kTrace>
-__device__ __forceinline__ void transport_body(const KernelArgs& A, unsigned char* smem) {
+__device__ __forceinline__ void transport_body(const KernelArgs& A) {
+  unsigned char* smem = vmc_smem;
   using Tr = RealTraits<Real>;
   constexpr bool kF32 = std::is_same<Real, float>::value;
   using Rng = Xs128p<kTrace>;

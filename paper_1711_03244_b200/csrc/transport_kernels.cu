@@ -10,12 +10,13 @@
 
 namespace vmc {
 
-// Occupancy: the plain FP32 kernel fits 48 registers without spills -> 5 CTAs
-// (40 warps) per SM; the gated / detector / trace variants carry more state and
-// are capped at 64 registers (4 CTAs). FP64 (parity mode) is unconstrained.
+// Occupancy: every FP32 variant is capped at 64 registers (4 CTAs = 32 warps per
+// SM). The plain kernel also fits 48 registers without spills (5 CTAs), which
+// measured 1-2 % slower: the loop is issue-bound, not latency-bound. FP64
+// (parity mode) is unconstrained.
 #ifndef VMC_MIN_BLOCKS
 #if VMC_REAL_IS_FLOAT
-#define VMC_MIN_BLOCKS_PLAIN 5
+#define VMC_MIN_BLOCKS_PLAIN 4
 #define VMC_MIN_BLOCKS_RICH 4
 #else
 #define VMC_MIN_BLOCKS_PLAIN 1
@@ -28,8 +29,7 @@ namespace vmc {
 template <typename Real, bool G, bool D, bool T>
 __global__ void __launch_bounds__(kBlock, (G || D || T) ? VMC_MIN_BLOCKS_RICH : VMC_MIN_BLOCKS_PLAIN)
     k_transport(const __grid_constant__ KernelArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  transport_body<Real, G, D, T>(A, smem);
+  transport_body<Real, G, D, T>(A);
 }
 
 #define VMC_CAT2(a, b) a##b

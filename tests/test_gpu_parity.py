@@ -231,3 +231,22 @@ def test_isotropic_source_diffusion_shape(gpu, ref):
     w = ref.walk(v.Scene(grid, src), cfg, 0, 100_000, threads=8, counts=True)
     assert g.totals.deposited / w["disp"][0] - 1 == pytest.approx(0, abs=2e-3)
     assert l2_rel(g.map.cw_cells(), w["cells"], w["counts"] >= 100) < 2e-2
+
+
+def test_run_multi_two_slots_peer_reduce(gpu):
+    """vmc_run_multi with two device slots on the same GPU: contiguous S3/S1
+    ranges, per-slot kernels, device-side peer reduce + detector gather/sort;
+    the merged map equals one run bit for bit (test_scheduler.cpp:246-264)."""
+    st = setup("b3", n=300_000)
+    devs = [gpu.DeviceProfile(name="a", cores=2, a=1e-6, t0=0.0, gpu=0),
+            gpu.DeviceProfile(name="b", cores=1, a=2e-6, t0=0.1, gpu=0)]
+    one = gpu.run_group_dynamic(0, 300_000, 1, st.scene, st.config)
+    for strat in (gpu.Strategy.S1, gpu.Strategy.S3):
+        m = gpu.run_multi_device(300_000, devs, strat, st.scene, st.config)
+        assert sum(m.partition.counts) == 300_000 and min(m.partition.counts) > 0
+        assert np.array_equal(m.map.cells, one.map.cells)
+        assert m.totals_q == one.totals_q
+        assert m.det_count == one.det_count
+        assert np.array_equal(m.detections["photon_index"], one.detections["photon_index"])
+        assert np.array_equal(m.detections["w_exit"], one.detections["w_exit"])
+        assert m.reduce_ms > 0
