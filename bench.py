@@ -277,6 +277,14 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "flop_per_photon": FLOP_PER_PHOTON[args.workload],
             "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz (SIMT FP32; neither HBM nor tensor bound)",
             "l2_atomics_per_s": ATOMICS_PER_PHOTON[args.workload] * mine / (kern_ms_per * 1e-3)}
+    # secondary: the HBM roofline the contract names, to show it does not bound
+    # this kernel (algorithmic bytes = labels + media + fluence map, read once)
+    alg_bytes = st.grid.voxel_count + len(st.grid.media) * 64 + plan.ncells * 8
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof["secondary"] = {"hbm": {"achieved": alg_bytes / (kern_ms_per * 1e-3) / 1e9, "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": alg_bytes / (kern_ms_per * 1e-3) / 1e9 / hbm_peak,
+                                 "algorithmic_bytes": alg_bytes,
+                                 "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}}
     prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         try:
