@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -180,7 +181,7 @@ std::vector<vmc::Medium<Real>> build_media(const vmc_scene* s) {
     std::memset(&M, 0, sizeof M);
     M.mua = static_cast<Real>(mua);
     M.mus = static_cast<Real>(mus);
-    M.inv_mus = mus > 0.0 ? static_cast<Real>(1.0 / mus) : Real(0);
+    M.inv_mus = mus > 0.0 ? static_cast<Real>(1.0 / mus) : std::numeric_limits<Real>::infinity();
     const double nspm = n * (1.0 / vmc::kLightMmPerNs);  // advance(), transport.cpp:169
     M.ns_per_mm = static_cast<Real>(nspm);
     M.mm_per_ns = static_cast<Real>(1.0 / nspm);

@@ -438,7 +438,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
     const int nlab_pf = static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
     Real d_s;
     if constexpr (kF32) {
-      d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();
+      d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
     } else {
       d_s = M.mus > 0.0 ? rs / M.mus : Tr::inf();
     }
