@@ -250,3 +250,66 @@ def test_run_multi_two_slots_peer_reduce(gpu):
         assert np.array_equal(m.detections["photon_index"], one.detections["photon_index"])
         assert np.array_equal(m.detections["w_exit"], one.detections["w_exit"])
         assert m.reduce_ms > 0
+
+
+def _corner_scene(kind):
+    """Small scenes that stress branches the BASELINE workloads rarely take."""
+    n = 20
+    lab = np.ones((n, n, n), np.uint8)
+    c = (np.arange(n) + 0.5) - n / 2
+    r2 = c[:, None, None] ** 2 + c[None, :, None] ** 2 + c[None, None, :] ** 2
+    air = v.OpticalProperties(0, 0, 0, 1.0)
+    cfg = v.SimulationConfig(photon_count=50_000, master_seed=9, tmax_ns=5.0,
+                             boundary_mode=v.BoundaryMode.ReflectAtMismatch)
+    src = v.Source((10.0, 10.0, 0.0), (0.0, 0.0, 1.0))
+    if kind == "roulette":  # strong absorption: weights fall below 1e-4 -> roulette
+        media = [air, v.OpticalProperties(0.3, 10.0, 0.0, 1.3)]
+    elif kind == "horizon":  # short time horizon: most photons truncated
+        media = [air, v.OpticalProperties(0.01, 2.0, 0.5, 1.4)]
+        cfg.tmax_ns = 0.05
+    elif kind == "backward":  # negative anisotropy, isotropic-branch medium inside
+        media = [air, v.OpticalProperties(0.02, 3.0, -0.5, 1.33), v.OpticalProperties(0.01, 1.0, 0.0, 1.33)]
+        lab[r2 <= 25] = 2
+    elif kind == "dense_inclusion":  # high-index sphere, refraction both ways + TIR inside
+        media = [air, v.OpticalProperties(0.005, 1.0, 0.8, 1.0), v.OpticalProperties(0.01, 4.0, 0.9, 1.6)]
+        lab[r2 <= 36] = 2
+    elif kind == "terminate_inner":  # terminate mode still resolves inner mismatches
+        media = [air, v.OpticalProperties(0.01, 1.0, 0.7, 1.37), v.OpticalProperties(0.01, 1.0, 0.7, 1.0)]
+        lab[r2 <= 36] = 2
+        cfg.boundary_mode = v.BoundaryMode.TerminateAtBoundary
+    elif kind == "oblique":  # oblique pencil off a voxel corner
+        media = [air, v.OpticalProperties(0.01, 1.0, 0.9, 1.37)]
+        src = v.Source((7.0, 9.0, 0.0), (0.3, -0.2, 0.9))
+    grid = v.VoxelGrid((n, n, n), 1.0, lab, media)
+    return v.Scene(grid, src), cfg
+
+
+CORNERS = ["roulette", "horizon", "backward", "dense_inclusion", "terminate_inner", "oblique"]
+
+
+@pytest.mark.parametrize("kind", CORNERS)
+def test_corner_fp64_per_photon(gpu, ref, kind):
+    scene, cfg = _corner_scene(kind)
+    cfg.precision = v.Precision.FP64
+    tr = gpu.trace_photons(scene, cfg, 0, 5000)
+    rt = ref.walk(scene, cfg, 0, 5000, threads=8, cells=False, traces=True)["traces"]
+    same = tr["draws"] == rt["draws"]
+    assert same.mean() >= 0.995
+    for f in ("deposited", "escaped", "killed", "truncated"):
+        assert np.abs(tr[f][same] - rt[f][same]).max() < 1e-6, f
+    assert np.array_equal(tr["flags"][same], rt["flags"][same])
+
+
+@pytest.mark.parametrize("kind", CORNERS)
+def test_corner_fp32_run(gpu, ref, kind):
+    scene, cfg = _corner_scene(kind)
+    g = gpu.run_group_dynamic(0, 50_000, 1, scene, cfg)
+    w = ref.walk(scene, cfg, 0, 50_000, threads=8, counts=True)
+    n = 50_000
+    assert abs(g.totals.books() - n) / n < 1e-6
+    for i, name in enumerate(("deposited", "escaped", "killed", "truncated")):
+        # correlated streams: channel totals agree to far below MC noise
+        assert abs(getattr(g.totals, name) - w["disp"][i]) <= 2e-3 * n + 1e-9, name
+    mask = w["counts"] >= 100
+    if mask.sum() > 10:
+        assert l2_rel(g.map.cw_cells(), w["cells"], mask) < 2e-2

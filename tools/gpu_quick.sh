@@ -1,3 +1,2 @@
 python paper_1711_03244_b200/build.py >/dev/null
-python tools/quick_tp.py 2>&1 | grep -E "tp"
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -6
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k corner 2>&1 | tail -25
