@@ -234,6 +234,16 @@ def run_group_dynamic(first_index: int, quota: int, threads: int, scene: Scene,
 run_static_split = run_group_dynamic
 
 
+def simulate_photon(photon_index: int, scene: Scene, config: SimulationConfig,
+                    device: int = 0):
+    """One photon's walk on the device (reference simulate_photon /
+    simulate_photon_trace, transport.cpp:362-380): returns its disposition and
+    its per-voxel deposits as a FluenceMap in the quantum of
+    config.photon_count."""
+    r = run_group_dynamic(photon_index, 1, 1, scene, config, device)
+    return r.totals, r.map
+
+
 # ---------------------------------------------------------------------------
 class DeviceKind(enum.Enum):
     RealWorkerPool = "pool"

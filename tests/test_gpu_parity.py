@@ -313,3 +313,22 @@ def test_corner_fp32_run(gpu, ref, kind):
     mask = w["counts"] >= 100
     if mask.sum() > 10:
         assert l2_rel(g.map.cw_cells(), w["cells"], mask) < 2e-2
+
+
+def test_simulate_photon_matches_reference_trace(gpu, ref):
+    """simulate_photon_trace (transport.cpp:368-380) for single photons, FP64 mode:
+    same per-voxel deposits as the reference's trace."""
+    st = v.benchmark_preset(v.Benchmark.B2)
+    st.config.master_seed = 1
+    st.config.precision = v.Precision.FP64
+    st.config.photon_count = 100_000
+    q = v.quantum_for(100_000)
+    for idx in (0, 1, 2, 12345):
+        disp, fmap = gpu.simulate_photon(idx, st.scene, st.config)
+        deps, rdisp = ref.trace(st.scene, st.config, idx)
+        want = np.zeros(st.grid.voxel_count, np.int64)
+        for cell, dw in deps:
+            want[cell] += int(round(dw / q))
+        got = fmap.cw_cells()
+        assert np.abs(got - want).max() <= 2  # llround ties / last-bit log differences
+        assert disp.deposited == pytest.approx(rdisp[0], rel=1e-9)
