@@ -345,9 +345,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   const bool gates = c->ngates > 1, det = c->ndet > 0;
   P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
   P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
-  // media table (16-byte aligned) + per-thread cold state (4 x u64 + 2 x Real per thread)
-  P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
-            static_cast<size_t>(vmc::kBlock) * (4 * sizeof(uint64_t) + 2 * (f64 ? sizeof(double) : sizeof(float)));
+  P->smem = media_bytes;  // the media table is K1's only shared-memory use
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");

@@ -166,7 +166,7 @@ struct Walk;
 // The kernel body (shared by both precisions).
 
 // Dynamic shared memory of K1, referenced through the symbol (not a generic
-// pointer) so every access compiles to LDS/STS with a constant window base.
+// pointer) so every access compiles to LDS with a constant window base.
 extern __shared__ __align__(16) unsigned char vmc_smem[];
 
 template <typename Real, bool kGates, bool kDet, bool kTrace>
@@ -176,21 +176,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   constexpr bool kF32 = std::is_same<Real, float>::value;
   using Rng = Xs128p<kTrace>;
 
-  // ---- shared memory: media table, then per-thread "cold" state (values
-  // touched only at photon end / azimuth retries / records), structure of
-  // arrays so each access is bank-conflict free; keeps the loop under 64 regs
+  // ---- shared memory: media table ---------------------------------------
   Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem);
-  unsigned char* cold = smem + ((sizeof(Medium<Real>) * A.nmedia + 15) & ~static_cast<size_t>(15));
-  const int tid = threadIdx.x;
-  long long* c_esc = reinterpret_cast<long long*>(cold) + tid;
-  long long* c_kill = c_esc + kBlock;
-  long long* c_trunc = c_kill + kBlock;
-  uint64_t* c_idx = reinterpret_cast<uint64_t*>(c_trunc + kBlock);
-  Real* c_sct = reinterpret_cast<Real*>(reinterpret_cast<uint64_t*>(cold) + 4 * kBlock) + tid;
-  Real* c_sst = c_sct + kBlock;
-  *c_esc = 0;
-  *c_kill = 0;
-  *c_trunc = 0;
   {
     const Medium<Real>* gm = static_cast<const Medium<Real>*>(A.media);
     const int nwords = static_cast<int>(sizeof(Medium<Real>) / 4) * A.nmedia;
@@ -212,14 +199,16 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
   // per-thread fixed-point disposition totals
-  long long acc_dep = 0;  // escaped/killed/truncated quanta live in shared memory (c_*)
+  long long acc_dep = 0, acc_esc = 0, acc_kill = 0, acc_trunc = 0;
 
   // photon state
   // 0 = ready to step, 1 = at a scattering point (scatter deferred to a scatter
   // phase), 2 = no photon (lane waits for a refill), 3 = scatter in progress,
   // waiting for another azimuth rejection-sampling try (ct/st kept in sct/sst)
   int phase = 2;
+  Real sct = 0, sst = 0;
   bool exhausted = false;  // warp-uniform: counter ran past `count`
+  uint64_t idx = 0;
   Rng rng;
   rng.a = rng.b = 0;
   Real px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, ix = 0, iy = 0, iz = 0;
@@ -285,13 +274,13 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       tr.escaped = pd_esc;
       tr.killed = pd_kill;
       tr.truncated = pd_trunc;
-      A.trace[*c_idx - A.first] = tr;
+      A.trace[idx - A.first] = tr;
     }
     if constexpr (!kF32) {
       acc_dep += llround(pd_dep * A.qscale);
-      *c_esc += llround(pd_esc * A.qscale);
-      *c_kill += llround(pd_kill * A.qscale);
-      *c_trunc += llround(pd_trunc * A.qscale);
+      acc_esc += llround(pd_esc * A.qscale);
+      acc_kill += llround(pd_kill * A.qscale);
+      acc_trunc += llround(pd_trunc * A.qscale);
     }
     phase = 2;
   };
@@ -317,8 +306,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
           const unsigned long long my = base + __popc(need & lanemask_lt);
           if (my < A.count) {
             // ---- launch, transport.cpp:83-106 ----
-            const uint64_t idx = A.first + my;
-            *c_idx = idx;
+            idx = A.first + my;
             rng.seed(A.seed, idx);
             Real ux, uy, uz;
             if (A.iso_source) {
@@ -490,7 +478,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
         const long long q = quant(run_w0 - w);
         deposit(cell, gate, vx, vy, vz, q);
         acc_dep += q;
-        *c_trunc += quant(w);
+        acc_trunc += quant(w);
       }
       pd_trunc += w;
       finish(2);
@@ -582,7 +570,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
         const long long q = quant(run_w0 - w);
         deposit(cell, gate, vx, vy, vz, q);
         acc_dep += q;
-        *c_esc += quant(w);
+        acc_esc += quant(w);
       }
       pd_esc += w;
       if constexpr (kDet) {
@@ -609,7 +597,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
             if (slot < A.det_cap) {
               unsigned char* rec = A.det_out + slot * static_cast<unsigned long long>(A.rec_stride);
               vmc_det_record_head hd;
-              hd.photon_index = *c_idx;
+              hd.photon_index = idx;
               hd.det_id = static_cast<uint32_t>(hit);
               hd.nscat = nscat;
               hd.w_exit = static_cast<float>(w);
@@ -689,8 +677,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
           } else {
             st = sqrt(fmax(0.0, 1.0 - ct * ct));
           }
-          *c_sct = ct;
-          *c_sst = st;
+          sct = ct;
+          sst = st;
           }
           // one try of the rejection azimuth (transport.cpp:32-44); a rejected
           // lane keeps ct/st and retries in the next scatter phase, so the warp
@@ -713,7 +701,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
             cp = ax_ * k;
             sp = ay_ * k;
           }
-          const Real ct = *c_sct, st = *c_sst;
+          const Real ct = sct, st = sst;
           Real ox, oy, oz;
           if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
             ox = st * cp;
@@ -765,13 +753,13 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
               acc_dep += q;
             }
             if (!survive) {
-              if constexpr (kF32) *c_kill += quant(before);
+              if constexpr (kF32) acc_kill += quant(before);
               pd_kill += before;
               finish(1);
             } else {
             w *= rmult;
             if constexpr (kF32) {
-              *c_kill += quant(before) - quant(w);
+              acc_kill += quant(before) - quant(w);
               run_w0 = w;
             }
             pd_kill += before - w;
@@ -787,7 +775,6 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   }
 
   // ---- epilogue: dispositions (warp reduce) -------------------------------
-  long long acc_esc = *c_esc, acc_kill = *c_kill, acc_trunc = *c_trunc;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     acc_dep += __shfl_xor_sync(0xffffffffu, acc_dep, o);

@@ -1,2 +1,9 @@
-python paper_1711_03244_b200/build.py >/dev/null
-timeout 900 python -m pytest tests/test_acceptance_gpu.py tests/test_gpu_parity.py -m gpu -q -k "c1 or c2 or c10 or c11 or simulate" 2>&1 | tail -25
+# A/B of transport.cuh variants in one session
+cp paper_1711_03244_b200/csrc/transport.cuh /tmp/transport_cur.cuh
+for var in cur regs_sym; do
+  if [ $var = cur ]; then cp /tmp/transport_cur.cuh paper_1711_03244_b200/csrc/transport.cuh; else cp tools/ab/transport_$var.cuh paper_1711_03244_b200/csrc/transport.cuh; fi
+  rm -f paper_1711_03244_b200/lib/obj/transport_f32.o paper_1711_03244_b200/lib/obj/transport_f64.o
+  python paper_1711_03244_b200/build.py > /dev/null 2>&1 || echo BUILD FAILED $var
+  echo "== $var"; python tools/quick_tp.py 2>&1 | grep tp
+done
+cp /tmp/transport_cur.cuh paper_1711_03244_b200/csrc/transport.cuh
