@@ -521,27 +521,27 @@ constexpr int kNcclSum = 0;    // ncclSum
 }  // namespace
 
 namespace {
-// K4: normalize (fluence.cpp:62-90). One thread per output cell; labels via
-// the read-only path, mua from a small constant-size table argument.
+// K4: normalize (fluence.cpp:62-90). HBM-streaming pass: one thread per voxel
+// (grid-stride), the voxel's 1/(mua V N) factor computed once and applied to
+// all of its gates; coalesced int64 loads and float stores, no integer division.
 __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* __restrict__ labels,
                             const double* __restrict__ mua, long long nvox, int ngates, int sum_gates,
                             int normalized, double scale, float* __restrict__ out) {
-  const long long n = sum_gates ? nvox : nvox * ngates;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long v = i % nvox;
-    long long raw = 0;
-    if (sum_gates) {
-      for (int g = 0; g < ngates; ++g) raw += cells[v + g * nvox];
-    } else {
-      raw = cells[i];
-    }
-    double val = static_cast<double>(raw) * scale;  // scale = quantum (/(V N) when normalized)
+  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvox;
+       v += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double f = scale;  // quantum (/(V N) when normalized)
     if (normalized) {
       const double m = mua[__ldg(labels + v)];
-      val = m > 0.0 ? val / m : 0.0;
+      f = m > 0.0 ? scale / m : 0.0;
     }
-    out[i] = static_cast<float>(val);
+    if (sum_gates) {
+      long long raw = 0;
+      for (int g = 0; g < ngates; ++g) raw += __ldcs(cells + v + g * nvox);
+      out[v] = static_cast<float>(static_cast<double>(raw) * f);
+    } else {
+      for (int g = 0; g < ngates; ++g)
+        __stcs(out + v + g * nvox, static_cast<float>(static_cast<double>(__ldcs(cells + v + g * nvox)) * f));
+    }
   }
 }
 
@@ -878,8 +878,9 @@ int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t photon_c
     const double q = vmc_quantum_for(plan->cfg.photon_count);
     const double v = plan->voxel_mm * plan->voxel_mm * plan->voxel_mm;
     const double scale = normalized ? q / (v * static_cast<double>(photon_count)) : q;
-    const long long n = sum_gates ? nvox : nvox * plan->cfg.ngates;
-    const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+    const int grid = static_cast<int>(std::min<long long>((nvox + 255) / 256, static_cast<long long>(sms) * 8));
     k_normalize<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const long long*>(d_cells), static_cast<const uint8_t*>(plan->labels.p),
         static_cast<const double*>(plan->mua.p), nvox, plan->cfg.ngates, sum_gates, normalized, scale, d_out);

@@ -1,9 +1,3 @@
-# A/B of transport.cuh variants in one session
-cp paper_1711_03244_b200/csrc/transport.cuh /tmp/transport_cur.cuh
-for var in cur regs_sym; do
-  if [ $var = cur ]; then cp /tmp/transport_cur.cuh paper_1711_03244_b200/csrc/transport.cuh; else cp tools/ab/transport_$var.cuh paper_1711_03244_b200/csrc/transport.cuh; fi
-  rm -f paper_1711_03244_b200/lib/obj/transport_f32.o paper_1711_03244_b200/lib/obj/transport_f64.o
-  python paper_1711_03244_b200/build.py > /dev/null 2>&1 || echo BUILD FAILED $var
-  echo "== $var"; python tools/quick_tp.py 2>&1 | grep tp
-done
-cp /tmp/transport_cur.cuh paper_1711_03244_b200/csrc/transport.cuh
+python paper_1711_03244_b200/build.py >/dev/null
+python tools/bench_k4.py
+timeout 600 python -m pytest tests -m gpu -q -k "normalize or pipeline" 2>&1 | tail -3
