@@ -539,8 +539,16 @@ __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* 
       for (int g = 0; g < ngates; ++g) raw += __ldcs(cells + v + g * nvox);
       out[v] = static_cast<float>(static_cast<double>(raw) * f);
     } else {
-      for (int g = 0; g < ngates; ++g)
-        __stcs(out + v + g * nvox, static_cast<float>(static_cast<double>(__ldcs(cells + v + g * nvox)) * f));
+      // issue up to 8 gate loads before the first store (memory-level parallelism)
+      for (int g0 = 0; g0 < ngates; g0 += 8) {
+        long long raw[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (g0 + k < ngates) raw[k] = __ldcs(cells + v + (g0 + k) * nvox);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (g0 + k < ngates) __stcs(out + v + (g0 + k) * nvox, static_cast<float>(static_cast<double>(raw[k]) * f));
+      }
     }
   }
 }
