@@ -28,8 +28,8 @@
 #include "transport.cuh"
 
 namespace vmc {
-const void* transport_kernel_float(bool gates, bool det, bool trace);
-const void* transport_kernel_double(bool gates, bool det, bool trace);
+const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
+const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
 namespace {
@@ -343,8 +343,17 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.det_cap = c->det_capacity;
 
   const bool gates = c->ngates > 1, det = c->ndet > 0;
-  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false) : vmc::transport_kernel_float(gates, det, false);
-  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true) : vmc::transport_kernel_float(gates, det, true);
+  bool uniform = true;  // single-label volume -> specialised kernel (identical results)
+  {
+    const uint8_t l0 = s->labels[0];
+    for (size_t i = 1; i < nvox && uniform; ++i) uniform = s->labels[i] == l0;
+    const char* ku = std::getenv("VMC_UNIFORM_FASTPATH");
+    if (ku && ku[0] == '0') uniform = false;
+  }
+  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false, uniform)
+                : vmc::transport_kernel_float(gates, det, false, uniform);
+  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true, uniform)
+                      : vmc::transport_kernel_float(gates, det, true, uniform);
   P->smem = media_bytes;  // the media table is K1's only shared-memory use
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");

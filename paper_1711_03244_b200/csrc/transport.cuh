@@ -169,7 +169,11 @@ struct Walk;
 // pointer) so every access compiles to LDS with a constant window base.
 extern __shared__ __align__(16) unsigned char vmc_smem[];
 
-template <typename Real, bool kGates, bool kDet, bool kTrace>
+// kUni: every voxel carries the same label (homogeneous phantoms such as the
+// cube60 benchmarks): an interior neighbour is then always the same medium,
+// so the neighbour-label load and refractive-class compare are skipped.
+// Results are identical to the general path.
+template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni = false>
 __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   unsigned char* smem = vmc_smem;
   using Tr = RealTraits<Real>;
@@ -423,7 +427,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
     const int nvax = vax + stp;
     const int ncell = stp > 0 ? cell + stride : cell - stride;
     const bool exterior = static_cast<unsigned>(nvax) >= static_cast<unsigned>(nax);
-    const int nlab_pf = static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
+    const int nlab_pf = kUni ? lab : static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
     Real d_s;
     if constexpr (kF32) {
       d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
@@ -517,7 +521,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       pz = axis == 2 ? plane : pz + dz * d;
     }
     const int nlab = exterior ? 0 : nlab_pf;
-    const int c1 = M.nclass, c2 = sm_media[nlab].nclass;
+    const int c1 = M.nclass, c2 = (kUni && !exterior) ? c1 : sm_media[nlab].nclass;
     bool move = false, exited = false;
     if (!exterior && c1 == c2) {
       move = true;  // same refractive index: inline update (transport.cpp:218-223)

@@ -26,19 +26,24 @@ namespace vmc {
 #define VMC_MIN_BLOCKS_PLAIN VMC_MIN_BLOCKS
 #define VMC_MIN_BLOCKS_RICH VMC_MIN_BLOCKS
 #endif
-template <typename Real, bool G, bool D, bool T>
+template <typename Real, bool G, bool D, bool T, bool U = false>
 __global__ void __launch_bounds__(kBlock, (G || D || T) ? VMC_MIN_BLOCKS_RICH : VMC_MIN_BLOCKS_PLAIN)
     k_transport(const __grid_constant__ KernelArgs A) {
-  transport_body<Real, G, D, T>(A);
+  transport_body<Real, G, D, T, U>(A);
 }
 
 #define VMC_CAT2(a, b) a##b
 #define VMC_CAT(a, b) VMC_CAT2(a, b)
 
-// Returns the kernel for (gates, detectors, trace); host code launches it with
-// cudaLaunchKernel and sizes the persistent grid by occupancy.
-const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trace) {
+// Returns the kernel for (gates, detectors, trace, single-label volume); host
+// code launches it with cudaLaunchKernel and sizes the persistent grid by
+// occupancy. The single-label specialisation exists for the plain and gated
+// production variants (detector / trace variants use the general path).
+const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trace, bool uniform) {
   using R = VMC_REAL;
+  if (uniform && !det && !trace)
+    return gates ? reinterpret_cast<const void*>(&k_transport<R, true, false, false, true>)
+                 : reinterpret_cast<const void*>(&k_transport<R, false, false, false, true>);
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
   switch (key) {
     case 0: return reinterpret_cast<const void*>(&k_transport<R, false, false, false>);
