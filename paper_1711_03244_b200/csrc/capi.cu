@@ -326,7 +326,6 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.error_flag = static_cast<int*>(P->err.p);
 
   A.hf = static_cast<float>(A.h);
-  A.inv_hf = static_cast<float>(1.0 / A.h);
   A.tmaxf = static_cast<float>(A.tmax);
   A.rthrf = static_cast<float>(A.rthr);
   A.rmultf = static_cast<float>(A.rmult);

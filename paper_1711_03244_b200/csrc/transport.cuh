@@ -25,9 +25,12 @@
 //
 // Fluence cells are int64 fixed point in the reference quantum
 // (proj/core/src/fluence.cpp:11-14); the device adds them with
-// red.global.add.u64, or into a per-CTA shared-memory "hot box" around the
-// source (native 32-bit shared atomics, lo/hi split with exact carry) that is
-// flushed once at kernel exit.
+// red.global.add.u64 (the map is L2-resident for the cube60 phantoms).
+//
+// Warp scheduling (see the loop below): scatters are deferred and run as a
+// warp phase once enough lanes wait, with one azimuth rejection try per phase;
+// dead lanes are refilled in groups. Photons are independent, so scheduling
+// never changes a photon's arithmetic or its RNG draw order.
 #pragma once
 
 #include <cstdint>
@@ -38,10 +41,6 @@
 
 namespace vmc {
 
-#ifndef VMC_SUBSTEPS
-#define VMC_SUBSTEPS 1
-#endif
-constexpr int kSubSteps = VMC_SUBSTEPS;  // steps per warp iteration before the scatter check
 constexpr int kBlock = 256;  // threads per CTA of K1
 constexpr int kMaxDet = 16;
 constexpr int kMaxDetMedia = 8;
@@ -80,7 +79,7 @@ struct KernelArgs {
   long long* cells;
   long long* totals;  // [4] deposited, escaped, killed, truncated quanta
   // float copies of the hot constants (no FP64 conversion inside the loop)
-  float hf, tmaxf, rthrf, rmultf, inv_rmultf, inv_gate_wf, qscalef, inv_hf;
+  float hf, tmaxf, rthrf, rmultf, inv_rmultf, inv_gate_wf, qscalef, pad4;
   // detectors
   int ndet, nppath, rec_stride, pad3;
   // warp scheduling: scatter phase when >= scatter_pct % of live lanes wait;
@@ -141,29 +140,6 @@ struct RealTraits<double> {
   static __device__ __forceinline__ double ln(double x) { return log(x); }
   static __device__ __forceinline__ double exp_neg(double x) { return exp(-x); }
 };
-
-// pick component `axis` of (x, y, z) without dynamic register indexing
-template <typename T>
-__device__ __forceinline__ T sel3(int axis, T x, T y, T z) {
-  return axis == 0 ? x : (axis == 1 ? y : z);
-}
-
-// 64-bit add into a shared-memory cell stored as two 32-bit words, with native
-// 32-bit shared atomics; the carry out of the low word is propagated exactly
-// once by the thread whose add wrapped it.
-__device__ __forceinline__ void smem_add_u64(unsigned int* lo, unsigned int* hi, unsigned long long v) {
-  const unsigned int vlo = static_cast<unsigned int>(v);
-  unsigned int vhi = static_cast<unsigned int>(v >> 32);
-  const unsigned int old = atomicAdd(lo, vlo);
-  vhi += (old + vlo < old) ? 1u : 0u;
-  if (vhi) atomicAdd(hi, vhi);
-}
-
-template <typename Real, bool kGates, bool kDet, bool kTrace>
-struct Walk;
-
-// ---------------------------------------------------------------------------
-// The kernel body (shared by both precisions).
 
 // Dynamic shared memory of K1, referenced through the symbol (not a generic
 // pointer) so every access compiles to LDS with a constant window base.
@@ -229,7 +205,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   for (int m = 0; m < (kDet ? kMaxDetMedia : 1); ++m) ppath[m] = 0;
 
   // one fixed-point add per deposit run (red.global.add.u64; the map is L2-resident)
-  auto deposit = [&](int c, int gt, int, int, int, long long q) {
+  auto deposit = [&](int c, int gt, long long q) {
     if (q != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt),
                 static_cast<unsigned long long>(q));
@@ -287,6 +263,361 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       acc_trunc += llround(pd_trunc * A.qscale);
     }
     phase = 2;
+  };
+
+  // one advance() step (transport.cpp:161-225) and the face / interface /
+  // exit handling that follows it in run_photon (transport.cpp:322-357)
+  auto step = [&]() {
+    // ---- one advance() step, transport.cpp:161-225 ----
+    const Medium<Real>& M = sm_media[lab];
+    if constexpr (kTrace) ++steps;
+    // boundary_distance, transport.cpp:49-73
+    Real tb0, tb1, tb2;
+    {
+      const Real plx = static_cast<Real>(vx + (dx > Real(0) ? 1 : 0)) * h;
+      const Real ply = static_cast<Real>(vy + (dy > Real(0) ? 1 : 0)) * h;
+      const Real plz = static_cast<Real>(vz + (dz > Real(0) ? 1 : 0)) * h;
+      const Real t0_ = (plx - px) * ix, t1_ = (ply - py) * iy, t2_ = (plz - pz) * iz;
+      tb0 = dx != Real(0) ? (t0_ > Real(0) ? t0_ : Real(0)) : Tr::inf();
+      tb1 = dy != Real(0) ? (t1_ > Real(0) ? t1_ : Real(0)) : Tr::inf();
+      tb2 = dz != Real(0) ? (t2_ > Real(0) ? t2_ : Real(0)) : Tr::inf();
+    }
+    // select-style argmin (ties -> lower axis), carrying the crossed axis'
+    // direction component, voxel coordinate, extent and cell stride along
+    int axis = 0;
+    Real d_b = tb0, dax = dx;
+    int vax = vx, nax = nx, stride = 1;
+    if (tb1 < d_b) {
+      d_b = tb1;
+      axis = 1;
+      dax = dy;
+      vax = vy;
+      nax = ny;
+      stride = nx;
+    }
+    if (tb2 < d_b) {
+      d_b = tb2;
+      axis = 2;
+      dax = dz;
+      vax = vz;
+      nax = nz;
+      stride = nxy32;
+    }
+    // neighbour across the nearest face; its label load is issued here so the
+    // L1/L2 latency overlaps the rest of the step (used only if the step crosses)
+    const int stp = dax > Real(0) ? 1 : -1;
+    const int nvax = vax + stp;
+    const int ncell = stp > 0 ? cell + stride : cell - stride;
+    const bool exterior = static_cast<unsigned>(nvax) >= static_cast<unsigned>(nax);
+    const int nlab_pf = kUni ? lab : static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
+    Real d_s;
+    if constexpr (kF32) {
+      d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
+    } else {
+      d_s = M.mus > 0.0 ? rs / M.mus : Tr::inf();
+    }
+    const Real ns = M.ns_per_mm;
+    const Real remaining = tmax - t;
+    Real d = d_b < d_s ? d_b : d_s;  // std::min(d_boundary, d_scatter)
+    const bool horizon = d * ns >= remaining;
+    if (horizon) {
+      if constexpr (kF32) {
+        d = fmaxf(0.0f, remaining * M.mm_per_ns);
+      } else {
+        d = fmax(0.0, remaining / ns);
+      }
+    }
+    // Beer-Lambert, exp_neg transport.cpp:22-27
+    Real w1;
+    {
+      const Real x = M.mua * d;
+      Real e;
+      const Real taylor = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
+      if constexpr (kF32) {
+        e = x < 0.01f ? taylor : Tr::exp_neg(x);  // branch-free select
+      } else {
+        e = x < 0.01 ? taylor : exp(-x);
+      }
+      w1 = w * e;
+    }
+    const Real t_start = t;
+    if constexpr (!kF32) {
+      // per-step deposit into the pre-step voxel (transport.cpp:323-327)
+      const Real dw = w - w1;
+      if (dw != 0.0) {
+        deposit(cell, gate_of(t_start), llround(dw * A.qscale));
+        pd_dep += dw;
+      }
+    } else if constexpr (kTrace) {
+      pd_dep += static_cast<double>(w - w1);
+    }
+    w = w1;
+    t += d * ns;
+    if constexpr (kDet) {
+#pragma unroll
+      for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] += (lab == m + 1) ? d : Real(0);
+    }
+
+    if (horizon) {  // StepKind::Terminated
+      t = tmax;
+      if constexpr (kF32) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, q);
+        acc_dep += q;
+        acc_trunc += quant(w);
+      }
+      pd_trunc += w;
+      finish(2);
+      return;
+    }
+
+    if (d_s <= d_b) {  // StepKind::Scattered: move to the scattering point
+      px += dx * d;
+      py += dy * d;
+      pz += dz * d;
+      if constexpr (kGates && kF32) {
+        const int ng = gate_of(t);
+        if (ng != gate) {
+          const long long q = quant(run_w0 - w);
+          deposit(cell, gate, q);
+          acc_dep += q;
+          run_w0 = w;
+          gate = ng;
+        }
+      }
+      phase = 1;  // hg_scatter + new length + roulette run in a scatter phase
+      return;
+    }
+
+    // ---- land exactly on the face (transport.cpp:197-211) ----
+    if constexpr (kF32) {
+      rs = fmaxf(0.0f, rs - d * M.mus);
+    } else {
+      rs = fmax(0.0, rs - d * M.mus);
+    }
+    {
+      // land exactly on the crossed plane; the other two coordinates advance
+      const Real plane = static_cast<Real>(vax + (stp > 0 ? 1 : 0)) * h;
+      px = axis == 0 ? plane : px + dx * d;
+      py = axis == 1 ? plane : py + dy * d;
+      pz = axis == 2 ? plane : pz + dz * d;
+    }
+    const int nlab = exterior ? 0 : nlab_pf;
+    const int c1 = M.nclass, c2 = (kUni && !exterior) ? c1 : sm_media[nlab].nclass;
+    bool move = false, exited = false;
+    if (!exterior && c1 == c2) {
+      move = true;  // same refractive index: inline update (transport.cpp:218-223)
+    } else if (exterior && !A.reflect) {
+      exited = true;  // TerminateAtBoundary (transport.cpp:234-237)
+    } else if (c1 == c2) {
+      exited = exterior;  // identity interface, n1 == n2 (transport.cpp:242-252)
+      move = !exterior;
+    } else {
+      // Fresnel / TIR, handle_interface transport.cpp:254-297
+      const Real n1 = M.n, n2 = sm_media[nlab].n;
+      const Real ci = dax < Real(0) ? -dax : dax;
+      Real si2 = Real(1) - ci * ci;
+      si2 = si2 > Real(0) ? si2 : Real(0);
+      const Real eta = n1 / n2;
+      const Real st2 = eta * eta * si2;
+      if (st2 > Real(1)) {  // total internal reflection: deterministic flip
+        set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
+      } else {
+        Real cost;
+        if constexpr (kF32) {
+          cost = sqrtf(1.0f - st2);
+        } else {
+          cost = sqrt(1.0 - st2);
+        }
+        const Real rsp = (n1 * ci - n2 * cost) / (n1 * ci + n2 * cost);
+        const Real rpp = (n1 * cost - n2 * ci) / (n1 * cost + n2 * ci);
+        const Real R = Real(0.5) * (rsp * rsp + rpp * rpp);
+        if (rng.template unit<Real>() < R) {
+          set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
+        } else {
+          Real qx = axis == 0 ? (dax > Real(0) ? cost : -cost) : dx * eta;
+          Real qy = axis == 1 ? (dax > Real(0) ? cost : -cost) : dy * eta;
+          Real qz = axis == 2 ? (dax > Real(0) ? cost : -cost) : dz * eta;
+          Real k;
+          if constexpr (kF32) {
+            k = Tr::rsqrt(qx * qx + qy * qy + qz * qz);
+          } else {
+            k = 1.0 / sqrt(qx * qx + qy * qy + qz * qz);
+          }
+          set_dir(qx * k, qy * k, qz * k);
+          exited = exterior;
+          move = !exterior;
+        }
+      }
+    }
+
+    if (exited) {  // ExitedDomain: escaped += w (transport.cpp:348-350)
+      if constexpr (kF32) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, q);
+        acc_dep += q;
+        acc_esc += quant(w);
+      }
+      pd_esc += w;
+      if constexpr (kDet) {
+        int hit = -1;
+        for (int k = 0; k < A.ndet; ++k) {
+          const double ex = static_cast<double>(px) - A.det[k][0];
+          const double ey = static_cast<double>(py) - A.det[k][1];
+          const double ez = static_cast<double>(pz) - A.det[k][2];
+          if (ex * ex + ey * ey + ez * ez <= A.det[k][3] * A.det[k][3]) {
+            hit = k;
+            break;
+          }
+        }
+        const unsigned am = __activemask();
+        const unsigned hm = __ballot_sync(am, hit >= 0);
+        if constexpr (kTrace) detected = hit >= 0;
+        if (hm) {
+          const int leader = __ffs(hm) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(A.det_count, static_cast<unsigned long long>(__popc(hm)));
+          base = __shfl_sync(am, base, leader);
+          if (hit >= 0) {
+            const unsigned long long slot = base + __popc(hm & lanemask_lt);
+            if (slot < A.det_cap) {
+              unsigned char* rec = A.det_out + slot * static_cast<unsigned long long>(A.rec_stride);
+              vmc_det_record_head hd;
+              hd.photon_index = idx;
+              hd.det_id = static_cast<uint32_t>(hit);
+              hd.nscat = nscat;
+              hd.w_exit = static_cast<float>(w);
+              hd.t_exit_ns = static_cast<float>(t);
+              *reinterpret_cast<vmc_det_record_head*>(rec) = hd;
+              float* pp = reinterpret_cast<float*>(rec + sizeof(vmc_det_record_head));
+#pragma unroll
+              for (int m = 0; m < kMaxDetMedia; ++m)
+                if (m < A.nppath) pp[m] = static_cast<float>(ppath[m]);
+            }
+          }
+        }
+      }
+      finish(0);
+      return;
+    }
+    if (move) {
+      if constexpr (kF32) {
+        const int ng = gate_of(t);
+        // a new voxel (or gate) closes the current deposit run
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, q);
+        acc_dep += q;
+        run_w0 = w;
+        gate = ng;
+      }
+      vx += axis == 0 ? stp : 0;
+      vy += axis == 1 ? stp : 0;
+      vz += axis == 2 ? stp : 0;
+      cell = ncell;
+      lab = nlab;
+    } else if constexpr (kGates && kF32) {
+      const int ng = gate_of(t);
+      if (ng != gate) {
+        const long long q = quant(run_w0 - w);
+        deposit(cell, gate, q);
+        acc_dep += q;
+        run_w0 = w;
+        gate = ng;
+      }
+    }
+  };
+
+  // hg_scatter (transport.cpp:126-147) + new free path (:14-17) + roulette
+  // (:300-306, called at :333-343) for a lane at a scattering point
+  auto scatter = [&]() {
+    const Medium<Real>& M = sm_media[lab];
+    if (phase == 1) {  // first visit: Henyey-Greenstein cos(theta) (transport.cpp:120-124)
+      if constexpr (kTrace || kDet) ++nscat;
+      const Real xi = rng.template unit<Real>();
+      Real ct;
+      if (M.iso) {
+        ct = Real(2) * xi - Real(1);
+      } else if constexpr (kF32) {
+        const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
+        ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
+      } else {
+        const double g = M.g;
+        const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
+        ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
+        ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
+      }
+      sct = ct;
+      if constexpr (kF32) {
+        sst = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
+      } else {
+        sst = sqrt(fmax(0.0, 1.0 - ct * ct));
+      }
+    }
+    // one try of the rejection azimuth (transport.cpp:32-44); a rejected lane
+    // keeps cos/sin(theta) and retries in the next scatter phase, so the warp
+    // never loops on its unluckiest lane
+    const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
+    const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
+    const Real r2 = ax_ * ax_ + ay_ * ay_;
+    if (!(r2 > Real(1e-12) && r2 <= Real(1))) {
+      phase = 3;
+      return;
+    }
+    phase = 0;
+    const Real k = Tr::rsqrt(r2);
+    const Real cp = ax_ * k, sp = ay_ * k;
+    const Real ct = sct, st = sst;
+    // rotate into the frame of the old direction (transport.cpp:133-141)
+    Real ox, oy, oz;
+    if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
+      ox = st * cp;
+      oy = st * sp;
+      oz = dz > Real(0) ? ct : -ct;
+    } else if constexpr (kF32) {
+      const float one_m = 1.0f - dz * dz;
+      const float rden = Tr::rsqrt(one_m);
+      const float sr = st * rden;
+      ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
+      oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
+      oz = -st * cp * (one_m * rden) + dz * ct;
+    } else {
+      const double den = sqrt(1.0 - dz * dz);
+      ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
+      oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
+      oz = -st * cp * den + dz * ct;
+    }
+    // renormalize (transport.cpp:142-145; 1e-6 in FP32, the reference's 1e-12 in FP64)
+    const Real n2 = ox * ox + oy * oy + oz * oz;
+    if ((n2 - Real(1) < Real(0) ? Real(1) - n2 : n2 - Real(1)) > (kF32 ? Real(1e-6) : Real(1e-12))) {
+      const Real kk = Tr::rsqrt(n2);
+      ox *= kk;
+      oy *= kk;
+      oz *= kk;
+    }
+    set_dir(ox, oy, oz);
+    rs = scat_len();
+    // roulette after a scatter only (transport.cpp:333-343, 300-306)
+    if (w < rthr) {
+      const Real before = w;
+      const bool survive = rng.template unit<Real>() < inv_rmult;
+      if constexpr (kF32) {
+        const long long q = quant(run_w0 - w);  // close the deposit run
+        deposit(cell, gate, q);
+        acc_dep += q;
+      }
+      if (!survive) {
+        if constexpr (kF32) acc_kill += quant(before);
+        pd_kill += before;
+        finish(1);
+        return;
+      }
+      w *= rmult;
+      if constexpr (kF32) {
+        acc_kill += quant(before) - quant(w);
+        run_w0 = w;
+      }
+      pd_kill += before - w;
+    }
   };
 
   unsigned dead = 0xffffffffu;  // lanes without a photon (warp-uniform view)
@@ -380,271 +711,9 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       if (exhausted) break;
       continue;
     }
-    // ---- step phase(s): every lane holding a photon that is not at a
-    // scattering point advances by up to kSubSteps steps before the scatter check
-#pragma unroll 1
-    for (int sub = 0; sub < kSubSteps; ++sub) {
-    do {
-    if (phase != 0) break;
-    // ---- one advance() step, transport.cpp:161-225 ----
-    const Medium<Real>& M = sm_media[lab];
-    if constexpr (kTrace) ++steps;
-    // boundary_distance, transport.cpp:49-73
-    Real tb0, tb1, tb2;
-    {
-      const Real plx = static_cast<Real>(vx + (dx > Real(0) ? 1 : 0)) * h;
-      const Real ply = static_cast<Real>(vy + (dy > Real(0) ? 1 : 0)) * h;
-      const Real plz = static_cast<Real>(vz + (dz > Real(0) ? 1 : 0)) * h;
-      const Real t0_ = (plx - px) * ix, t1_ = (ply - py) * iy, t2_ = (plz - pz) * iz;
-      tb0 = dx != Real(0) ? (t0_ > Real(0) ? t0_ : Real(0)) : Tr::inf();
-      tb1 = dy != Real(0) ? (t1_ > Real(0) ? t1_ : Real(0)) : Tr::inf();
-      tb2 = dz != Real(0) ? (t2_ > Real(0) ? t2_ : Real(0)) : Tr::inf();
-    }
-    // select-style argmin (ties -> lower axis), carrying the crossed axis'
-    // direction component, voxel coordinate, extent and cell stride along
-    int axis = 0;
-    Real d_b = tb0, dax = dx;
-    int vax = vx, nax = nx, stride = 1;
-    if (tb1 < d_b) {
-      d_b = tb1;
-      axis = 1;
-      dax = dy;
-      vax = vy;
-      nax = ny;
-      stride = nx;
-    }
-    if (tb2 < d_b) {
-      d_b = tb2;
-      axis = 2;
-      dax = dz;
-      vax = vz;
-      nax = nz;
-      stride = nxy32;
-    }
-    // neighbour across the nearest face; its label load is issued here so the
-    // L1/L2 latency overlaps the rest of the step (used only if the step crosses)
-    const int stp = dax > Real(0) ? 1 : -1;
-    const int nvax = vax + stp;
-    const int ncell = stp > 0 ? cell + stride : cell - stride;
-    const bool exterior = static_cast<unsigned>(nvax) >= static_cast<unsigned>(nax);
-    const int nlab_pf = kUni ? lab : static_cast<int>(__ldg(A.labels + (exterior ? cell : ncell)));
-    Real d_s;
-    if constexpr (kF32) {
-      d_s = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
-    } else {
-      d_s = M.mus > 0.0 ? rs / M.mus : Tr::inf();
-    }
-    const Real ns = M.ns_per_mm;
-    const Real remaining = tmax - t;
-    Real d = d_b < d_s ? d_b : d_s;  // std::min(d_boundary, d_scatter)
-    const bool horizon = d * ns >= remaining;
-    if (horizon) {
-      if constexpr (kF32) {
-        d = fmaxf(0.0f, remaining * M.mm_per_ns);
-      } else {
-        d = fmax(0.0, remaining / ns);
-      }
-    }
-    // Beer-Lambert, exp_neg transport.cpp:22-27
-    Real w1;
-    {
-      const Real x = M.mua * d;
-      Real e;
-      const Real taylor = Real(1) - x * (Real(1) - x * (Real(0.5) - x * (Real(1.0 / 6.0) - x * Real(1.0 / 24.0))));
-      if constexpr (kF32) {
-        e = x < 0.01f ? taylor : Tr::exp_neg(x);  // branch-free select
-      } else {
-        e = x < 0.01 ? taylor : exp(-x);
-      }
-      w1 = w * e;
-    }
-    const Real t_start = t;
-    if constexpr (!kF32) {
-      // per-step deposit into the pre-step voxel (transport.cpp:323-327)
-      const Real dw = w - w1;
-      if (dw != 0.0) {
-        deposit(cell, gate_of(t_start), vx, vy, vz, llround(dw * A.qscale));
-        pd_dep += dw;
-      }
-    } else if constexpr (kTrace) {
-      pd_dep += static_cast<double>(w - w1);
-    }
-    w = w1;
-    t += d * ns;
-    if constexpr (kDet) {
-#pragma unroll
-      for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] += (lab == m + 1) ? d : Real(0);
-    }
-
-    if (horizon) {  // StepKind::Terminated
-      t = tmax;
-      if constexpr (kF32) {
-        const long long q = quant(run_w0 - w);
-        deposit(cell, gate, vx, vy, vz, q);
-        acc_dep += q;
-        acc_trunc += quant(w);
-      }
-      pd_trunc += w;
-      finish(2);
-      break;
-    }
-
-    if (d_s <= d_b) {  // StepKind::Scattered: move to the scattering point
-      px += dx * d;
-      py += dy * d;
-      pz += dz * d;
-      if constexpr (kGates && kF32) {
-        const int ng = gate_of(t);
-        if (ng != gate) {
-          const long long q = quant(run_w0 - w);
-          deposit(cell, gate, vx, vy, vz, q);
-          acc_dep += q;
-          run_w0 = w;
-          gate = ng;
-        }
-      }
-      phase = 1;  // hg_scatter + new length + roulette run in a scatter phase
-      break;
-    }
-
-    // ---- land exactly on the face (transport.cpp:197-211) ----
-    if constexpr (kF32) {
-      rs = fmaxf(0.0f, rs - d * M.mus);
-    } else {
-      rs = fmax(0.0, rs - d * M.mus);
-    }
-    {
-      // land exactly on the crossed plane; the other two coordinates advance
-      const Real plane = static_cast<Real>(vax + (stp > 0 ? 1 : 0)) * h;
-      px = axis == 0 ? plane : px + dx * d;
-      py = axis == 1 ? plane : py + dy * d;
-      pz = axis == 2 ? plane : pz + dz * d;
-    }
-    const int nlab = exterior ? 0 : nlab_pf;
-    const int c1 = M.nclass, c2 = (kUni && !exterior) ? c1 : sm_media[nlab].nclass;
-    bool move = false, exited = false;
-    if (!exterior && c1 == c2) {
-      move = true;  // same refractive index: inline update (transport.cpp:218-223)
-    } else if (exterior && !A.reflect) {
-      exited = true;  // TerminateAtBoundary (transport.cpp:234-237)
-    } else if (c1 == c2) {
-      exited = exterior;  // identity interface, n1 == n2 (transport.cpp:242-252)
-      move = !exterior;
-    } else {
-      // Fresnel / TIR, handle_interface transport.cpp:254-297
-      const Real n1 = M.n, n2 = sm_media[nlab].n;
-      const Real ci = dax < Real(0) ? -dax : dax;
-      Real si2 = Real(1) - ci * ci;
-      si2 = si2 > Real(0) ? si2 : Real(0);
-      const Real eta = n1 / n2;
-      const Real st2 = eta * eta * si2;
-      if (st2 > Real(1)) {  // total internal reflection: deterministic flip
-        set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
-      } else {
-        Real cost;
-        if constexpr (kF32) {
-          cost = sqrtf(1.0f - st2);
-        } else {
-          cost = sqrt(1.0 - st2);
-        }
-        const Real rsp = (n1 * ci - n2 * cost) / (n1 * ci + n2 * cost);
-        const Real rpp = (n1 * cost - n2 * ci) / (n1 * cost + n2 * ci);
-        const Real R = Real(0.5) * (rsp * rsp + rpp * rpp);
-        if (rng.template unit<Real>() < R) {
-          set_dir(axis == 0 ? -dx : dx, axis == 1 ? -dy : dy, axis == 2 ? -dz : dz);
-        } else {
-          Real qx = axis == 0 ? (dax > Real(0) ? cost : -cost) : dx * eta;
-          Real qy = axis == 1 ? (dax > Real(0) ? cost : -cost) : dy * eta;
-          Real qz = axis == 2 ? (dax > Real(0) ? cost : -cost) : dz * eta;
-          Real k;
-          if constexpr (kF32) {
-            k = Tr::rsqrt(qx * qx + qy * qy + qz * qz);
-          } else {
-            k = 1.0 / sqrt(qx * qx + qy * qy + qz * qz);
-          }
-          set_dir(qx * k, qy * k, qz * k);
-          exited = exterior;
-          move = !exterior;
-        }
-      }
-    }
-
-    if (exited) {  // ExitedDomain: escaped += w (transport.cpp:348-350)
-      if constexpr (kF32) {
-        const long long q = quant(run_w0 - w);
-        deposit(cell, gate, vx, vy, vz, q);
-        acc_dep += q;
-        acc_esc += quant(w);
-      }
-      pd_esc += w;
-      if constexpr (kDet) {
-        int hit = -1;
-        for (int k = 0; k < A.ndet; ++k) {
-          const double ex = static_cast<double>(px) - A.det[k][0];
-          const double ey = static_cast<double>(py) - A.det[k][1];
-          const double ez = static_cast<double>(pz) - A.det[k][2];
-          if (ex * ex + ey * ey + ez * ez <= A.det[k][3] * A.det[k][3]) {
-            hit = k;
-            break;
-          }
-        }
-        const unsigned am = __activemask();
-        const unsigned hm = __ballot_sync(am, hit >= 0);
-        if constexpr (kTrace) detected = hit >= 0;
-        if (hm) {
-          const int leader = __ffs(hm) - 1;
-          unsigned long long base = 0;
-          if (lane == leader) base = atomicAdd(A.det_count, static_cast<unsigned long long>(__popc(hm)));
-          base = __shfl_sync(am, base, leader);
-          if (hit >= 0) {
-            const unsigned long long slot = base + __popc(hm & lanemask_lt);
-            if (slot < A.det_cap) {
-              unsigned char* rec = A.det_out + slot * static_cast<unsigned long long>(A.rec_stride);
-              vmc_det_record_head hd;
-              hd.photon_index = idx;
-              hd.det_id = static_cast<uint32_t>(hit);
-              hd.nscat = nscat;
-              hd.w_exit = static_cast<float>(w);
-              hd.t_exit_ns = static_cast<float>(t);
-              *reinterpret_cast<vmc_det_record_head*>(rec) = hd;
-              float* pp = reinterpret_cast<float*>(rec + sizeof(vmc_det_record_head));
-#pragma unroll
-              for (int m = 0; m < kMaxDetMedia; ++m)
-                if (m < A.nppath) pp[m] = static_cast<float>(ppath[m]);
-            }
-          }
-        }
-      }
-      finish(0);
-      break;
-    }
-    if (move) {
-      if constexpr (kF32) {
-        const int ng = gate_of(t);
-        // a new voxel (or gate) closes the current deposit run
-        const long long q = quant(run_w0 - w);
-        deposit(cell, gate, vx, vy, vz, q);
-        acc_dep += q;
-        run_w0 = w;
-        gate = ng;
-      }
-      vx += axis == 0 ? stp : 0;
-      vy += axis == 1 ? stp : 0;
-      vz += axis == 2 ? stp : 0;
-      cell = ncell;
-      lab = nlab;
-    } else if constexpr (kGates && kF32) {
-      const int ng = gate_of(t);
-      if (ng != gate) {
-        const long long q = quant(run_w0 - w);
-        deposit(cell, gate, vx, vy, vz, q);
-        acc_dep += q;
-        run_w0 = w;
-        gate = ng;
-      }
-    }
-    } while (0);
-    }
+    // ---- step phase: every lane holding a photon that is not at a scattering
+    // point advances by one step (two steps per iteration measured slower)
+    if (phase == 0) step();
     // ---- scatter phase: run the deferred scatters once at least half of the
     // lanes holding a photon are at a scattering point (or nobody can step) ----
     {
@@ -652,128 +721,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       dead = __ballot_sync(0xffffffffu, phase == 2);
       const unsigned live = ~dead;
       if (pend != 0u && (pend == live || 100 * __popc(pend) >= A.scatter_pct * __popc(live))) {
-      if (phase & 1) {
-          {
-          // ---- scatter: hg_scatter (transport.cpp:126-147), new length ----
-          const Medium<Real>& M = sm_media[lab];
-          if (phase == 1) {
-          if constexpr (kTrace || kDet) ++nscat;
-          Real ct;
-          {
-            const Real xi = rng.template unit<Real>();
-            if (M.iso) {
-              ct = Real(2) * xi - Real(1);
-            } else {
-              if constexpr (kF32) {
-                const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
-                ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
-              } else {
-                const double g = M.g;
-                const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
-                ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
-                ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
-              }
-            }
-          }
-          Real st;
-          if constexpr (kF32) {
-            st = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
-          } else {
-            st = sqrt(fmax(0.0, 1.0 - ct * ct));
-          }
-          sct = ct;
-          sst = st;
-          }
-          // one try of the rejection azimuth (transport.cpp:32-44); a rejected
-          // lane keeps ct/st and retries in the next scatter phase, so the warp
-          // never loops on its unluckiest lane
-          Real cp, sp;
-          const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
-          const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
-          const Real r2 = ax_ * ax_ + ay_ * ay_;
-          if (!(r2 > Real(1e-12) && r2 <= Real(1))) {
-            phase = 3;
-          } else {
-          phase = 0;
-          {
-            Real k;
-            if constexpr (kF32) {
-              k = Tr::rsqrt(r2);
-            } else {
-              k = 1.0 / sqrt(r2);
-            }
-            cp = ax_ * k;
-            sp = ay_ * k;
-          }
-          const Real ct = sct, st = sst;
-          Real ox, oy, oz;
-          if ((dz < Real(0) ? -dz : dz) > Real(0.99999)) {
-            ox = st * cp;
-            oy = st * sp;
-            oz = dz > Real(0) ? ct : -ct;
-          } else {
-            if constexpr (kF32) {
-              const float one_m = 1.0f - dz * dz;
-              const float rden = Tr::rsqrt(one_m);
-              const float den = one_m * rden;
-              const float sr = st * rden;
-              ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
-              oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
-              oz = -st * cp * den + dz * ct;
-            } else {
-              const double den = sqrt(1.0 - dz * dz);
-              ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
-              oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
-              oz = -st * cp * den + dz * ct;
-            }
-          }
-          {
-            const Real n2 = ox * ox + oy * oy + oz * oz;
-            if constexpr (kF32) {
-              if (fabsf(n2 - 1.0f) > 1e-6f) {
-                const float k = Tr::rsqrt(n2);
-                ox *= k;
-                oy *= k;
-                oz *= k;
-              }
-            } else {
-              if (fabs(n2 - 1.0) > 1e-12) {
-                const double k = 1.0 / sqrt(n2);
-                ox *= k;
-                oy *= k;
-                oz *= k;
-              }
-            }
-          }
-          set_dir(ox, oy, oz);
-          rs = scat_len();
-          // roulette after a scatter only (transport.cpp:333-343, 300-306)
-          if (w < rthr) {
-            const Real before = w;
-            const bool survive = rng.template unit<Real>() < inv_rmult;
-            if constexpr (kF32) {
-              const long long q = quant(run_w0 - w);
-              deposit(cell, gate, vx, vy, vz, q);
-              acc_dep += q;
-            }
-            if (!survive) {
-              if constexpr (kF32) acc_kill += quant(before);
-              pd_kill += before;
-              finish(1);
-            } else {
-            w *= rmult;
-            if constexpr (kF32) {
-              acc_kill += quant(before) - quant(w);
-              run_w0 = w;
-            }
-            pd_kill += before - w;
-            }
-          }
-          }  // azimuth accepted
-          }
-
-      }
-      dead = __ballot_sync(0xffffffffu, phase == 2);  // roulette may have killed
+        if (phase & 1) scatter();
+        dead = __ballot_sync(0xffffffffu, phase == 2);  // roulette may have killed
       }
     }
   }
