@@ -333,7 +333,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   A.inv_gate_wf = static_cast<float>(A.inv_gate_w);
   A.qscalef = static_cast<float>(A.qscale);
   A.scatter_pct = env_int("VMC_SCATTER_PCT", 50);
-  A.refill_min = env_int("VMC_REFILL_MIN", 2);
+  A.refill_min = env_int("VMC_REFILL_MIN", 1);  // measured: 1 >= 2 > 3 > 4
   A.ndet = c->ndet;
   A.nppath = std::max(0, s->nmedia - 1);
   A.rec_stride = static_cast<int>(P->rec_stride);
