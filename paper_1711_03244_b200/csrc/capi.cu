@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -206,26 +207,61 @@ std::vector<vmc::Medium<Real>> build_media(const vmc_scene* s) {
   return out;
 }
 
+// Device allocation. Owning by default; `borrow` points at a cached buffer
+// (RangeCache) that outlives the call, so nothing is freed.
 struct DevBuf {
   void* p = nullptr;
   int dev = -1;
+  size_t cap = 0;
+  bool owned = true;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() {
-    if (p) {
+  ~DevBuf() { release(); }
+  void release() {
+    if (p && owned) {
       int cur = -1;
       cudaGetDevice(&cur);
       if (dev >= 0 && cur != dev) cudaSetDevice(dev);
       cudaFree(p);
       if (dev >= 0 && cur >= 0 && cur != dev) cudaSetDevice(cur);
     }
+    p = nullptr;
+    cap = 0;
   }
   void alloc(size_t bytes, int device) {
+    release();
     dev = device;
-    ck(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+    owned = true;
+    cap = bytes ? bytes : 16;
+    ck(cudaMalloc(&p, cap), "cudaMalloc");
+  }
+  // grow-only: keep the allocation when it is large enough
+  void ensure(size_t bytes, int device) {
+    if (!p || cap < bytes || dev != device) alloc(bytes, device);
+  }
+  void borrow(const DevBuf& from) {
+    release();
+    p = from.p;
+    dev = from.dev;
+    cap = from.cap;
+    owned = false;
   }
 };
+
+// Per-device buffers reused across vmc_run_range calls: cudaMalloc/cudaFree
+// churn (measured 10-700 ms of host time per call on B200 boxes) is kept out
+// of the executor; the scene itself is still uploaded on every call.
+struct RangeCache {
+  std::mutex mu;
+  DevBuf labels, media, mua, claim, err, cells, totals, det, detn;
+};
+
+RangeCache& range_cache(int device) {
+  static RangeCache* caches = new RangeCache[64];  // never destroyed: no cudaFree after CUDA teardown
+  if (device < 0 || device >= 64) fail_validation("device index out of range");
+  return caches[device];
+}
 
 }  // namespace
 
@@ -248,7 +284,7 @@ struct vmc_plan {
 
 namespace {
 
-void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device) {
+void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device, RangeCache* cache = nullptr) {
   validate(s, c);
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -265,30 +301,38 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device)
   P->ncells = static_cast<uint64_t>(nvox) * static_cast<uint64_t>(c->ngates);
   P->rec_stride = vmc_det_record_bytes(s->nmedia);
 
-  P->labels.alloc(nvox, device);
+  auto get = [&](DevBuf& own, DevBuf* shared, size_t bytes) {
+    if (shared) {
+      shared->ensure(bytes, device);
+      own.borrow(*shared);
+    } else {
+      own.alloc(bytes, device);
+    }
+  };
+  get(P->labels, cache ? &cache->labels : nullptr, nvox);
   ck(cudaMemcpy(P->labels.p, s->labels, nvox, cudaMemcpyHostToDevice), "upload labels");
   const bool f64 = c->precision == VMC_PRECISION_FP64;
   size_t media_bytes;
   if (f64) {
     auto m = build_media<double>(s);
     media_bytes = m.size() * sizeof(m[0]);
-    P->media.alloc(media_bytes, device);
+    get(P->media, cache ? &cache->media : nullptr, media_bytes);
     ck(cudaMemcpy(P->media.p, m.data(), media_bytes, cudaMemcpyHostToDevice), "upload media");
   } else {
     auto m = build_media<float>(s);
     media_bytes = m.size() * sizeof(m[0]);
-    P->media.alloc(media_bytes, device);
+    get(P->media, cache ? &cache->media : nullptr, media_bytes);
     ck(cudaMemcpy(P->media.p, m.data(), media_bytes, cudaMemcpyHostToDevice), "upload media");
   }
   {
     std::vector<double> mua(static_cast<size_t>(s->nmedia));
     for (int m = 0; m < s->nmedia; ++m) mua[m] = s->media[4 * m];
-    P->mua.alloc(mua.size() * sizeof(double), device);
+    get(P->mua, cache ? &cache->mua : nullptr, mua.size() * sizeof(double));
     ck(cudaMemcpy(P->mua.p, mua.data(), mua.size() * sizeof(double), cudaMemcpyHostToDevice), "upload mua");
   }
   P->voxel_mm = s->voxel_mm;
-  P->claim.alloc(sizeof(unsigned long long), device);
-  P->err.alloc(sizeof(int), device);
+  get(P->claim, cache ? &cache->claim : nullptr, sizeof(unsigned long long));
+  get(P->err, cache ? &cache->err : nullptr, sizeof(int));
   ck(cudaMemset(P->err.p, 0, sizeof(int)), "cudaMemset");
 
   vmc::KernelArgs& A = P->args;
@@ -434,26 +478,48 @@ struct RangeResult {
   double ms = 0.0;
 };
 
+// VMC_DEBUG_TIMING=1 prints the host-side phases of vmc_run_range to stderr.
+struct PhaseClock {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  PhaseClock() : on(std::getenv("VMC_DEBUG_TIMING") != nullptr) { t0 = last = std::chrono::steady_clock::now(); }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[vmc] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
+
 void run_range_device(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count, int device,
                       int64_t* cells_out, int64_t* totals_out, unsigned char* det_out, uint64_t* det_count_out,
                       double* ms_out) {
+  PhaseClock clk;
+  RangeCache& C = range_cache(device);
+  std::lock_guard<std::mutex> lock(C.mu);  // one in-flight call per device
   vmc_plan P;
-  plan_init(&P, s, c, device);
-  DevBuf cells, totals, det, detn;
-  cells.alloc(P.ncells * sizeof(int64_t), device);
-  totals.alloc(4 * sizeof(int64_t), device);
+  plan_init(&P, s, c, device, &C);
+  clk.mark("plan_init");
   const uint64_t cap = c->ndet > 0 ? c->det_capacity : 0;
-  det.alloc(cap * P.rec_stride, device);
-  detn.alloc(sizeof(uint64_t), device);
+  C.cells.ensure(P.ncells * sizeof(int64_t), device);
+  C.totals.ensure(4 * sizeof(int64_t), device);
+  C.det.ensure(cap * P.rec_stride, device);
+  C.detn.ensure(sizeof(uint64_t), device);
+  DevBuf& cells = C.cells;
+  DevBuf& totals = C.totals;
+  DevBuf& det = C.det;
+  DevBuf& detn = C.detn;
   cudaStream_t st;
   ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "event");
   ck(cudaEventCreate(&e1), "event");
+  clk.mark("alloc");
   try {
     ck(cudaEventRecord(e0, st), "event record");
     plan_enqueue(&P, first, count, static_cast<int64_t*>(cells.p), static_cast<int64_t*>(totals.p), det.p,
                  static_cast<uint64_t*>(detn.p), st, VMC_RUN_ZERO, false, nullptr);
+    clk.mark("enqueue");
     ck(cudaEventRecord(e1, st), "event record");
     if (cells_out)
       ck(cudaMemcpyAsync(cells_out, cells.p, P.ncells * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "download");
@@ -461,6 +527,7 @@ void run_range_device(const vmc_scene* s, const vmc_config* c, uint64_t first, u
     uint64_t n = 0;
     ck(cudaMemcpyAsync(&n, detn.p, sizeof n, cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "run");
+    clk.mark("sync");
     if (c->ndet > 0) {
       const uint64_t keep = std::min(n, cap);
       if (det_out && keep) {
@@ -482,6 +549,7 @@ void run_range_device(const vmc_scene* s, const vmc_config* c, uint64_t first, u
   cudaStreamDestroy(st);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  clk.mark("finish");
 }
 
 // ---- NCCL, loaded on demand (only vmc_run_multi with ndev > 1 needs it) ----
