@@ -597,33 +597,65 @@ constexpr int kNcclSum = 0;    // ncclSum
 }  // namespace
 
 namespace {
-// K4: normalize (fluence.cpp:62-90). HBM-streaming pass: one thread per voxel
-// (grid-stride), the voxel's 1/(mua V N) factor computed once and applied to
-// all of its gates; coalesced int64 loads and float stores, no integer division.
+// K4: normalize (fluence.cpp:62-90). HBM-streaming pass: each thread handles a
+// PAIR of consecutive voxels (16-byte int64x2 loads, 8-byte float2 stores),
+// computes the per-voxel 1/(mua V N) factor once and applies it to all gates;
+// up to 8 gate loads are in flight before the first store. No integer division.
 __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* __restrict__ labels,
                             const double* __restrict__ mua, long long nvox, int ngates, int sum_gates,
                             int normalized, double scale, float* __restrict__ out) {
-  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvox;
-       v += static_cast<long long>(gridDim.x) * blockDim.x) {
-    double f = scale;  // quantum (/(V N) when normalized)
-    if (normalized) {
-      const double m = mua[__ldg(labels + v)];
-      f = m > 0.0 ? scale / m : 0.0;
+  const long long npair = nvox >> 1;
+  const bool vec = (nvox & 1) == 0;  // pairs never straddle a gate boundary
+  const long long nwork = vec ? npair : nvox;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nwork;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int per = vec ? 2 : 1;
+    const long long v0 = i * per;
+    double f[2] = {scale, scale};
+    for (int j = 0; j < per; ++j) {
+      if (normalized) {
+        const double m = mua[__ldg(labels + v0 + j)];
+        f[j] = m > 0.0 ? scale / m : 0.0;
+      }
     }
     if (sum_gates) {
-      long long raw = 0;
-      for (int g = 0; g < ngates; ++g) raw += __ldcs(cells + v + g * nvox);
-      out[v] = static_cast<float>(static_cast<double>(raw) * f);
+      long long raw[2] = {0, 0};
+      for (int g = 0; g < ngates; ++g) {
+        if (vec) {
+          const longlong2 c = __ldcs(reinterpret_cast<const longlong2*>(cells + v0 + g * nvox));
+          raw[0] += c.x;
+          raw[1] += c.y;
+        } else {
+          raw[0] += __ldcs(cells + v0 + g * nvox);
+        }
+      }
+      if (vec)
+        __stcs(reinterpret_cast<float2*>(out + v0), make_float2(static_cast<float>(static_cast<double>(raw[0]) * f[0]),
+                                                                static_cast<float>(static_cast<double>(raw[1]) * f[1])));
+      else
+        out[v0] = static_cast<float>(static_cast<double>(raw[0]) * f[0]);
     } else {
-      // issue up to 8 gate loads before the first store (memory-level parallelism)
       for (int g0 = 0; g0 < ngates; g0 += 8) {
-        long long raw[8];
+        longlong2 buf[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (g0 + k < ngates) raw[k] = __ldcs(cells + v + (g0 + k) * nvox);
+        for (int k = 0; k < 8; ++k) {
+          if (g0 + k < ngates) {
+            if (vec) buf[k] = __ldcs(reinterpret_cast<const longlong2*>(cells + v0 + (g0 + k) * nvox));
+            else buf[k] = make_longlong2(__ldcs(cells + v0 + (g0 + k) * nvox), 0);
+          }
+        }
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (g0 + k < ngates) __stcs(out + v + (g0 + k) * nvox, static_cast<float>(static_cast<double>(raw[k]) * f));
+        for (int k = 0; k < 8; ++k) {
+          if (g0 + k < ngates) {
+            const float a = static_cast<float>(static_cast<double>(buf[k].x) * f[0]);
+            if (vec) {
+              const float b = static_cast<float>(static_cast<double>(buf[k].y) * f[1]);
+              __stcs(reinterpret_cast<float2*>(out + v0 + (g0 + k) * nvox), make_float2(a, b));
+            } else {
+              __stcs(out + v0 + (g0 + k) * nvox, a);
+            }
+          }
+        }
       }
     }
   }
@@ -964,7 +996,8 @@ int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t photon_c
     const double scale = normalized ? q / (v * static_cast<double>(photon_count)) : q;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
-    const int grid = static_cast<int>(std::min<long long>((nvox + 255) / 256, static_cast<long long>(sms) * 8));
+    const long long work = (nvox & 1) ? nvox : nvox / 2;  // voxel pairs when nvox is even
+    const int grid = static_cast<int>(std::min<long long>((work + 255) / 256, static_cast<long long>(sms) * 16));
     k_normalize<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const long long*>(d_cells), static_cast<const uint8_t*>(plan->labels.p),
         static_cast<const double*>(plan->mua.p), nvox, plan->cfg.ngates, sum_gates, normalized, scale, d_out);

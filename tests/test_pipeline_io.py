@@ -110,3 +110,30 @@ def test_run_pipeline_and_normalize(gpu, tmp_path):
     r.map.normalize(st.grid)
     host = r.map.to_float_volume()
     assert np.allclose(phi.cpu().numpy(), host, rtol=1e-6, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,ngates", [((5, 7, 9), 3), ((4, 6, 8), 10)])
+def test_normalize_kernel_odd_even_gates(gpu, dims, ngates):
+    """K4 on odd / even voxel counts (pair-vectorised and scalar paths), per gate and CW."""
+    import torch
+    nx, ny, nz = dims
+    rng = np.random.default_rng(3)
+    lab = rng.integers(1, 3, nx * ny * nz).astype(np.uint8)
+    media = [v.OpticalProperties(), v.OpticalProperties(0.02, 1.0, 0.5, 1.3), v.OpticalProperties(0.0, 1.0, 0.5, 1.3)]
+    grid = v.VoxelGrid(dims, 0.5, lab, media)
+    cfg = v.SimulationConfig(photon_count=12345, ngates=ngates)
+    scene = v.Scene(grid, v.Source((1.0, 1.0, 0.0), (0.0, 0.0, 1.0)))
+    plan = gpu.Plan(scene, cfg)
+    cells = rng.integers(0, 1 << 40, plan.ncells).astype(np.int64)
+    tc = torch.from_numpy(cells).cuda()
+    per = torch.zeros(plan.ncells, dtype=torch.float32, device="cuda")
+    cw = torch.zeros(grid.voxel_count, dtype=torch.float32, device="cuda")
+    plan.normalize_torch(tc, per, 12345, sum_gates=False)
+    plan.normalize_torch(tc, cw, 12345, sum_gates=True)
+    torch.cuda.synchronize()
+    fm = v.FluenceMap(dims, 12345, ngates, cells)
+    fm.normalize(grid)
+    assert np.allclose(per.cpu().numpy(), fm._values.reshape(-1).astype(np.float32), rtol=1e-6)
+    assert np.allclose(cw.cpu().numpy(), fm._values.sum(axis=0).reshape(-1).astype(np.float32), rtol=1e-5)
+    assert np.all(per.cpu().numpy().reshape(ngates, -1)[:, lab == 2] == 0)  # mua == 0 -> 0

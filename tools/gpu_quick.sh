@@ -1,3 +1,3 @@
 python paper_1711_03244_b200/build.py >/dev/null
-VMC_DEBUG_TIMING=1 python tools/e2e_probe.py 2>&1 | grep -v "^\[vmc\] \(alloc\|enqueue\|finish\)" | tail -30
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+python tools/bench_k4.py
+timeout 600 python -m pytest tests -m gpu -q -k "normalize or pipeline" 2>&1 | tail -3
