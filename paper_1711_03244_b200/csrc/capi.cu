@@ -397,7 +397,9 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
                 : vmc::transport_kernel_float(gates, det, false, uniform);
   P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true, uniform)
                       : vmc::transport_kernel_float(gates, det, true, uniform);
-  P->smem = media_bytes;  // the media table is K1's only shared-memory use
+  // media table, plus per-thread per-label path lengths in detector mode
+  P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
+            (det ? static_cast<size_t>(vmc::kMaxDetMedia) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float)) : 0);
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");

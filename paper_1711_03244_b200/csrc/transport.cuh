@@ -200,9 +200,19 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // per-photon (double path / trace)
   uint32_t steps = 0, nscat = 0;
   bool detected = false;
-  Real ppath[kDet ? kMaxDetMedia : 1];
-#pragma unroll
-  for (int m = 0; m < (kDet ? kMaxDetMedia : 1); ++m) ppath[m] = 0;
+  // detector mode: path length in the current medium accumulates in `seg` and
+  // is flushed into this thread's per-label slots in shared memory
+  // (pp_sm[m * kBlock + tid], bank-conflict free) only when the label changes
+  // or the photon exits, so a step costs one add
+  Real seg = 0;
+  Real* pp_sm = reinterpret_cast<Real*>(smem + ((sizeof(Medium<Real>) * A.nmedia + 15) & ~static_cast<size_t>(15))) +
+                threadIdx.x;
+  auto flush_seg = [&]() {
+    if constexpr (kDet) {
+      if (lab >= 1) pp_sm[(lab - 1) * kBlock] += seg;
+      seg = 0;
+    }
+  };
 
   // one fixed-point add per deposit run (red.global.add.u64; the map is L2-resident)
   auto deposit = [&](int c, int gt, long long q) {
@@ -353,10 +363,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
     }
     w = w1;
     t += d * ns;
-    if constexpr (kDet) {
-#pragma unroll
-      for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] += (lab == m + 1) ? d : Real(0);
-    }
+    if constexpr (kDet) seg += d;
 
     if (horizon) {  // StepKind::Terminated
       t = tmax;
@@ -460,6 +467,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       }
       pd_esc += w;
       if constexpr (kDet) {
+        flush_seg();
         int hit = -1;
         for (int k = 0; k < A.ndet; ++k) {
           const double ex = static_cast<double>(px) - A.det[k][0];
@@ -490,9 +498,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
               hd.t_exit_ns = static_cast<float>(t);
               *reinterpret_cast<vmc_det_record_head*>(rec) = hd;
               float* pp = reinterpret_cast<float*>(rec + sizeof(vmc_det_record_head));
-#pragma unroll
-              for (int m = 0; m < kMaxDetMedia; ++m)
-                if (m < A.nppath) pp[m] = static_cast<float>(ppath[m]);
+              for (int m = 0; m < A.nppath; ++m) pp[m] = static_cast<float>(pp_sm[m * kBlock]);
             }
           }
         }
@@ -514,6 +520,9 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
       vy += axis == 1 ? stp : 0;
       vz += axis == 2 ? stp : 0;
       cell = ncell;
+      if constexpr (kDet) {
+        if (nlab != lab) flush_seg();
+      }
       lab = nlab;
     } else if constexpr (kGates && kF32) {
       const int ng = gate_of(t);
@@ -698,8 +707,8 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
             steps = nscat = 0;
             pd_dep = pd_esc = pd_kill = pd_trunc = 0;
             if constexpr (kDet) {
-#pragma unroll
-              for (int m = 0; m < kMaxDetMedia; ++m) ppath[m] = 0;
+              seg = 0;
+              for (int m = 0; m < A.nppath; ++m) pp_sm[m * kBlock] = Real(0);
             }
             phase = 0;
           }
