@@ -12,3 +12,6 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transport -s 1 -c 1 -o gpurun_out/prof_b2_$TAG python tools/ncu_target.py b2 1e7 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -1 gpurun_out/ncu_full_$TAG.log
 cp paper_1711_03244_b200/lib/obj/transport_f32.o gpurun_out/transport_f32_$TAG.o
+for W in b1 b3 head; do
+  timeout 400 python bench.py --workload $W 2>&1 | tail -1 | tee gpurun_out/bench_${W}_$TAG.json
+done
