@@ -289,7 +289,13 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                roof["traffic"] = json.load(f).get(args.workload)
+                pj = json.load(f)
+            roof["traffic"] = pj.get(args.workload)
+            # issue-slot roofline of the same kernel (what actually bounds it):
+            # ncu IPC vs the 4 warp-instructions/cycle/SM issue peak, plus SIMT lanes
+            if args.workload in pj.get("issue", {}):
+                roof["secondary"]["issue"] = dict(pj["issue"][args.workload],
+                                                  source="profiles/r1_ncu_traffic_%s.csv" % args.workload)
         except Exception:
             pass
     cpu = None

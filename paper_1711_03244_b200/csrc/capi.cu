@@ -6,6 +6,7 @@
 // entry points (vmc_run_range / vmc_run_multi) are the drop-in for
 // run_group_dynamic / run_multi_device (proj/core/src/scheduler.cpp:255-451).
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -252,9 +253,15 @@ struct DevBuf {
 // Per-device buffers reused across vmc_run_range calls: cudaMalloc/cudaFree
 // churn (measured 10-700 ms of host time per call on B200 boxes) is kept out
 // of the executor; the scene itself is still uploaded on every call.
+// Scratch of the on-device detector-record sort (sort_records_device).
+struct RecSort {
+  DevBuf k0, k1, v0, v1, tmp, out;
+};
+
 struct RangeCache {
   std::mutex mu;
   DevBuf labels, media, mua, claim, err, cells, totals, det, detn;
+  RecSort rs;
 };
 
 RangeCache& range_cache(int device) {
@@ -455,7 +462,7 @@ void check_launch_errors(vmc_plan* P) {
 }
 
 // Sort packed detector records by photon index (deterministic output for any
-// device count / claim order).
+// device count / claim order). Host fallback for ranges wider than 2^32.
 void sort_records(unsigned char* recs, uint64_t n, size_t stride) {
   if (n < 2) return;
   std::vector<uint64_t> order(n);
@@ -469,6 +476,57 @@ void sort_records(unsigned char* recs, uint64_t n, size_t stride) {
   std::vector<unsigned char> tmp(n * stride);
   for (uint64_t i = 0; i < n; ++i) std::memcpy(tmp.data() + i * stride, recs + order[i] * stride, stride);
   std::memcpy(recs, tmp.data(), n * stride);
+}
+
+__global__ void k_rec_keys(const unsigned char* __restrict__ recs, uint32_t n, uint32_t stride, uint64_t first,
+                           uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    keys[i] = static_cast<uint32_t>(*reinterpret_cast<const uint64_t*>(recs + static_cast<size_t>(i) * stride) - first);
+    idx[i] = i;
+  }
+}
+
+// one 32-bit word per thread: record r = w / words_per_record (stride % 4 == 0)
+__global__ void k_rec_gather(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                             const uint32_t* __restrict__ order, uint64_t nwords, uint32_t wpr) {
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = w / wpr, k = w - r * wpr;
+    dst[w] = src[static_cast<uint64_t>(order[r]) * wpr + k];
+  }
+}
+
+// Sort n records (photon indices in [first, first + count), count <= 2^32) on
+// the device: radix sort of the 32-bit index offsets (only the bits count
+// needs) carrying record positions, then a gather into R.out. Returns R.out.
+const void* sort_records_device(const void* d_recs, uint64_t n, size_t stride, uint64_t first, uint64_t count,
+                                RecSort& R, int device, cudaStream_t st) {
+  if (n < 2) return d_recs;
+  const uint32_t n32 = static_cast<uint32_t>(n);
+  R.k0.ensure(n * 4, device);
+  R.k1.ensure(n * 4, device);
+  R.v0.ensure(n * 4, device);
+  R.v1.ensure(n * 4, device);
+  R.out.ensure(n * stride, device);
+  int end_bit = 1;
+  while (end_bit < 32 && (count - 1) >> end_bit) ++end_bit;
+  auto* k0 = static_cast<uint32_t*>(R.k0.p);
+  auto* k1 = static_cast<uint32_t*>(R.k1.p);
+  auto* v0 = static_cast<uint32_t*>(R.v0.p);
+  auto* v1 = static_cast<uint32_t*>(R.v1.p);
+  size_t tb = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, static_cast<int>(n32), 0, end_bit, st), "cub sort");
+  R.tmp.ensure(tb, device);
+  k_rec_keys<<<(n32 + 255) / 256, 256, 0, st>>>(static_cast<const unsigned char*>(d_recs), n32,
+                                                 static_cast<uint32_t>(stride), first, k0, v0);
+  ck(cub::DeviceRadixSort::SortPairs(R.tmp.p, tb, k0, k1, v0, v1, static_cast<int>(n32), 0, end_bit, st), "cub sort");
+  const uint64_t nwords = n * (stride / 4);
+  const int grid = static_cast<int>(std::min<uint64_t>((nwords + 255) / 256, 148ull * 16));
+  k_rec_gather<<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(d_recs), static_cast<uint32_t*>(R.out.p), v1, nwords,
+                                     static_cast<uint32_t>(stride / 4));
+  ck(cudaGetLastError(), "record sort");
+  return R.out.p;
 }
 
 // ---- one device, host buffers ---------------------------------------------
@@ -533,8 +591,14 @@ void run_range_device(const vmc_scene* s, const vmc_config* c, uint64_t first, u
     if (c->ndet > 0) {
       const uint64_t keep = std::min(n, cap);
       if (det_out && keep) {
-        ck(cudaMemcpy(det_out, det.p, keep * P.rec_stride, cudaMemcpyDeviceToHost), "download det");
-        sort_records(det_out, keep, P.rec_stride);
+        if (count <= (1ull << 32) && P.rec_stride % 4 == 0 && keep < (1ull << 31)) {
+          const void* sorted = sort_records_device(det.p, keep, P.rec_stride, first, count, C.rs, device, st);
+          ck(cudaMemcpyAsync(det_out, sorted, keep * P.rec_stride, cudaMemcpyDeviceToHost, st), "download det");
+          ck(cudaStreamSynchronize(st), "sort det");
+        } else {
+          ck(cudaMemcpy(det_out, det.p, keep * P.rec_stride, cudaMemcpyDeviceToHost), "download det");
+          sort_records(det_out, keep, P.rec_stride);
+        }
       }
     }
     if (det_count_out) *det_count_out = c->ndet > 0 ? n : 0;
@@ -758,6 +822,7 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
     struct Slot {
       std::unique_ptr<vmc_plan> plan;
       DevBuf cells, totals, det, detn;
+      RecSort rs;
       cudaStream_t st = nullptr;
       double ms = 0.0;
       uint64_t ndet = 0;
@@ -895,6 +960,7 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
       }
       // detector records: gather in device order, then sort by photon index
       uint64_t total_det = 0, stored = 0;
+      bool host_sort = false;
       for (int i = 0; i < ndev; ++i) {
         total_det += slot[i].ndet;
         const uint64_t keep = std::min(slot[i].ndet, cap);
@@ -903,14 +969,22 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
           const uint64_t take = std::min(keep, room);
           if (take) {
             cudaSetDevice(devices[i]);
-            ck(cudaMemcpy(static_cast<unsigned char*>(det_out) + stored * stride, slot[i].det.p, take * stride,
-                          cudaMemcpyDeviceToHost),
+            // each device sorts its own records; ranges ascend in device order,
+            // so the concatenation is sorted by photon index
+            const bool dev_sort = counts[i] <= (1ull << 32) && stride % 4 == 0 && keep < (1ull << 31);
+            if (!dev_sort) host_sort = true;
+            const void* src = dev_sort ? sort_records_device(slot[i].det.p, keep, stride, first[i], counts[i],
+                                                             slot[i].rs, devices[i], slot[i].st)
+                                       : slot[i].det.p;
+            ck(cudaMemcpyAsync(static_cast<unsigned char*>(det_out) + stored * stride, src, take * stride,
+                               cudaMemcpyDeviceToHost, slot[i].st),
                "download det");
+            ck(cudaStreamSynchronize(slot[i].st), "download det");
             stored += take;
           }
         }
       }
-      if (det_out) sort_records(static_cast<unsigned char*>(det_out), stored, stride);
+      if (det_out && host_sort) sort_records(static_cast<unsigned char*>(det_out), stored, stride);
       if (det_count_out) *det_count_out = config->ndet > 0 ? total_det : 0;
       for (int i = 0; i < ndev; ++i)
         if (per_device_ms) per_device_ms[i] = slot[i].ms;
