@@ -399,6 +399,12 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     for (size_t i = 1; i < nvox && uniform; ++i) uniform = s->labels[i] == l0;
     const char* ku = std::getenv("VMC_UNIFORM_FASTPATH");
     if (ku && ku[0] == '0') uniform = false;
+    if (uniform && l0 < s->nmedia) {
+      A.uni_f = build_media<float>(s)[l0];
+      A.uni_d = build_media<double>(s)[l0];
+    } else {
+      uniform = false;
+    }
   }
   P->kern = f64 ? vmc::transport_kernel_double(gates, det, false, uniform)
                 : vmc::transport_kernel_float(gates, det, false, uniform);

@@ -91,6 +91,10 @@ struct KernelArgs {
   unsigned long long det_cap;
   vmc_photon_trace* trace;
   int* error_flag;  // set to 1 when a launch point falls outside the grid
+  // single-label volumes (kUni): the one interior medium, read straight from
+  // the parameter bank (constant operands, no shared-memory address math)
+  Medium<float> uni_f;
+  Medium<double> uni_d;
 };
 
 // ---------------------------------------------------------------------------
@@ -155,6 +159,18 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   using Tr = RealTraits<Real>;
   constexpr bool kF32 = std::is_same<Real, float>::value;
   using Rng = Xs128p<kTrace>;
+  // optical data of the photon's current medium
+  auto medium = [&](int l) -> const Medium<Real>& {
+    if constexpr (kUni) {
+      if constexpr (kF32) {
+        return A.uni_f;
+      } else {
+        return A.uni_d;
+      }
+    } else {
+      return reinterpret_cast<const Medium<Real>*>(smem)[l];
+    }
+  };
 
   // ---- shared memory: media table ---------------------------------------
   Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem);
@@ -279,7 +295,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   // exit handling that follows it in run_photon (transport.cpp:322-357)
   auto step = [&]() {
     // ---- one advance() step, transport.cpp:161-225 ----
-    const Medium<Real>& M = sm_media[lab];
+    const Medium<Real>& M = medium(lab);
     if constexpr (kTrace) ++steps;
     // boundary_distance, transport.cpp:49-73
     Real tb0, tb1, tb2;
@@ -539,7 +555,7 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   // hg_scatter (transport.cpp:126-147) + new free path (:14-17) + roulette
   // (:300-306, called at :333-343) for a lane at a scattering point
   auto scatter = [&]() {
-    const Medium<Real>& M = sm_media[lab];
+    const Medium<Real>& M = medium(lab);
     if (phase == 1) {  // first visit: Henyey-Greenstein cos(theta) (transport.cpp:120-124)
       if constexpr (kTrace || kDet) ++nscat;
       const Real xi = rng.template unit<Real>();

@@ -1,3 +1,3 @@
 python paper_1711_03244_b200/build.py >/dev/null || exit 1
+python tools/quick_tp.py 2>&1 | grep tp
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 400 python bench.py --workload b3 --no-cpu-baseline 2>&1 | tail -1
