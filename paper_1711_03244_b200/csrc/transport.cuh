@@ -42,6 +42,9 @@
 namespace vmc {
 
 constexpr int kBlock = 256;  // threads per CTA of K1
+#ifndef VMC_AZ_UNROLL
+#define VMC_AZ_UNROLL 2  // azimuth rejection tries per scatter phase (unrolled; 2 measured best)
+#endif
 constexpr int kMaxDet = 16;
 constexpr int kMaxDetMedia = 8;
 constexpr double kLightMmPerNs = 299.792458;  // types.hpp:16
@@ -581,10 +584,18 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
     // one try of the rejection azimuth (transport.cpp:32-44); a rejected lane
     // keeps cos/sin(theta) and retries in the next scatter phase, so the warp
     // never loops on its unluckiest lane
-    const Real ax_ = Real(2) * rng.template unit<Real>() - Real(1);
-    const Real ay_ = Real(2) * rng.template unit<Real>() - Real(1);
-    const Real r2 = ax_ * ax_ + ay_ * ay_;
-    if (!(r2 > Real(1e-12) && r2 <= Real(1))) {
+    Real ax_ = 0, ay_ = 0, r2 = 0;
+    bool ok = false;
+#pragma unroll
+    for (int k = 0; k < VMC_AZ_UNROLL; ++k) {
+      if (k == 0 || !ok) {
+        ax_ = Real(2) * rng.template unit<Real>() - Real(1);
+        ay_ = Real(2) * rng.template unit<Real>() - Real(1);
+        r2 = ax_ * ax_ + ay_ * ay_;
+        ok = r2 > Real(1e-12) && r2 <= Real(1);
+      }
+    }
+    if (!ok) {
       phase = 3;
       return;
     }
