@@ -164,7 +164,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     import torch.distributed as dist
 
     import paper_1711_03244_b200 as v
-    from paper_1711_03244_b200.distributed import rank_ranges, reduce_to_root
+    from paper_1711_03244_b200.distributed import rank_ranges, reduce_to_root, run_group_distributed
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -246,8 +246,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            res = v.run_group_dynamic(first, mine, 1, st.scene, ecfg, device=local_rank,
-                                      cells_out=pinned_cells, det_out=pinned_det)
+            if world == 1:  # the reference-facing C-ABI call (vmc_run_range), host buffers
+                res = v.run_group_dynamic(first, mine, 1, st.scene, ecfg, device=local_rank,
+                                          cells_out=pinned_cells, det_out=pinned_det)
+            else:  # per rank: scene upload + transport, NCCL reduce, merged map to rank-0 host
+                run_group_distributed(st.scene, ecfg, total, device=local_rank, cells_out=pinned_cells)
             t1 = time.perf_counter()
             if i > 0:
                 times.append(t1 - t0)
@@ -255,11 +258,18 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         nm = len(st.grid.media)
-        h2d = st.grid.voxel_count + nm * 4 * 8 + len(ecfg.detectors) * 32
-        d2h = plan.ncells * 8 + 4 * 8 + (min(res.det_count, ecfg.det_capacity) * plan.rec_bytes if ecfg.detectors else 0)
+        h2d = (st.grid.voxel_count + nm * 4 * 8 + len(ecfg.detectors) * 32) * world  # scene, every rank
+        if world == 1:
+            d2h = plan.ncells * 8 + 4 * 8 + (min(res.det_count, ecfg.det_capacity) * plan.rec_bytes
+                                             if ecfg.detectors else 0)
+        else:
+            d2h = plan.ncells * 8 + 4 * 8  # merged map + dispositions on rank 0
         e2e = {"value": total / (float(tt[0]) * 1e3), "unit": "photons/ms", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "path": "run_group_dynamic -> vmc_run_range (scene upload, kernel, map + records download into pinned host buffers), wall clock"}
+               "path": ("run_group_dynamic -> vmc_run_range (scene upload, kernel, map + records download into pinned "
+                        "host buffers), wall clock" if world == 1 else
+                        "distributed.run_group_distributed per rank (scene upload, kernel, NCCL reduce, merged map "
+                        "download to rank-0 pinned host buffer), wall clock, max over ranks")}
 
     if rank != 0:
         return

@@ -334,3 +334,14 @@ def test_simulate_photon_matches_reference_trace(gpu, ref):
         assert np.all(np.abs(got - want) <= 1e-9 * np.abs(want) + 2)
         assert np.array_equal(got > 0, want > 0)  # same voxels visited
         assert disp.deposited == pytest.approx(rdisp[0], rel=1e-9)
+
+
+def test_run_group_distributed_single_process_matches(gpu):
+    """distributed.run_group_distributed (plan + reduce + root download) with no
+    process group == run_group_dynamic over the same range (integer maps)."""
+    from paper_1711_03244_b200.distributed import run_group_distributed
+    st = v.baseline_setup("b2", photons=200_000)
+    cells, tq = run_group_distributed(st.scene, st.config)
+    r = gpu.run_group_dynamic(0, 200_000, 1, st.scene, st.config)
+    assert np.array_equal(cells.reshape(-1), r.map.cells.reshape(-1))
+    assert tuple(tq) == tuple(r.totals_q)
