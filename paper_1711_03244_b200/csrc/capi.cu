@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <map>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -656,11 +657,27 @@ Nccl& nccl() {
   return n;
 }
 
+
 void nck(int r, const char* what) {
   if (r != 0) {
     Nccl& n = nccl();
     fail_runtime(std::string(what) + ": " + (n.GetErrorString ? n.GetErrorString(r) : "nccl error"));
   }
+}
+
+// Communicators per device list, created once (ncclCommInitAll costs far more
+// than a cube60 reduce) and kept for the life of the process.
+std::vector<void*>& nccl_comms(const int* devices, int ndev) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::vector<void*>>* cache = new std::map<std::vector<int>, std::vector<void*>>;
+  std::lock_guard<std::mutex> lock(mu);
+  std::vector<int> key(devices, devices + ndev);
+  auto it = cache->find(key);
+  if (it != cache->end()) return it->second;
+  Nccl& N = nccl();
+  std::vector<void*> comms(ndev, nullptr);
+  nck(N.CommInitAll(comms.data(), ndev, devices), "ncclCommInitAll");
+  return cache->emplace(std::move(key), std::move(comms)).first->second;
 }
 
 constexpr int kNcclInt64 = 4;  // ncclInt64
@@ -921,8 +938,9 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
       } else if (ndev > 1) {
         // one exchange step: NCCL reduce of the int64 maps + totals onto devices[0]
         Nccl& N = nccl();
-        std::vector<void*> comms(ndev, nullptr);
-        nck(N.CommInitAll(comms.data(), ndev, devices), "ncclCommInitAll");
+        static std::mutex reduce_mu;  // cached communicators: one reduce at a time
+        std::lock_guard<std::mutex> reduce_lock(reduce_mu);
+        std::vector<void*>& comms = nccl_comms(devices, ndev);
         cudaSetDevice(devices[0]);
         cudaEvent_t r0, r1;
         ck(cudaEventCreate(&r0), "event");
@@ -949,8 +967,6 @@ int vmc_run_multi(const vmc_scene* scene, const vmc_config* config, int ndev, co
         red_ms = ms;
         cudaEventDestroy(r0);
         cudaEventDestroy(r1);
-        for (int i = 0; i < ndev; ++i)
-          if (N.CommDestroy) N.CommDestroy(comms[i]);
       }
       cudaSetDevice(devices[0]);
       if (cells_out)
