@@ -33,7 +33,7 @@ UNITS = [
     ("voxmc_api.cpp", "voxmc_api.o", []),
 ]
 
-HEADERS = ["transport.cuh", "rng.cuh", "partition.hpp"]
+HEADERS = ["transport.cuh", "flight.cuh", "rng.cuh", "partition.hpp"]
 
 
 def _stale(obj: str, src: str) -> bool:

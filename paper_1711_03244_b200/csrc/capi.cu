@@ -33,6 +33,7 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
 namespace {
@@ -407,10 +408,29 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
       uniform = false;
     }
   }
-  P->kern = f64 ? vmc::transport_kernel_double(gates, det, false, uniform)
-                : vmc::transport_kernel_float(gates, det, false, uniform);
-  P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true, uniform)
-                      : vmc::transport_kernel_float(gates, det, true, uniform);
+  A.inv_nxf = 1.0f / static_cast<float>(s->nx);
+  A.inv_nxyf = 1.0f / static_cast<float>(A.nxy);
+  A.event_pct = env_int("VMC_EVENT_PCT", 80);  // measured: 80 >= 90 > 60
+  {
+    double mx = 0.0;
+    for (int m = 0; m < s->nmedia; ++m) mx = std::max(mx, s->media[4 * m]);
+    const double xmax = mx * s->voxel_mm * std::sqrt(3.0);
+    A.absorb_mode = xmax < 0.012 ? 0 : (xmax < 0.15 ? 1 : 2);
+  }
+  // FP32: K1f (flight.cuh) unless VMC_KERNEL=step selects the per-step K1
+  // (transport.cuh) for A/B runs; FP64 parity mode always runs K1.
+  const char* kk = std::getenv("VMC_KERNEL");
+  const bool step_kernel = kk && std::strcmp(kk, "step") == 0;
+  if (f64) {
+    P->kern = vmc::transport_kernel_double(gates, det, false, uniform);
+    P->kern_trace = vmc::transport_kernel_double(gates, det, true, uniform);
+  } else if (step_kernel) {
+    P->kern = vmc::transport_kernel_float(gates, det, false, uniform);
+    P->kern_trace = vmc::transport_kernel_float(gates, det, true, uniform);
+  } else {
+    P->kern = vmc::flight_kernel_float(gates, det, false, uniform);
+    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform);
+  }
   // media table, plus per-thread per-label path lengths in detector mode
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
             (det ? static_cast<size_t>(vmc::kMaxDetMedia) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float)) : 0);

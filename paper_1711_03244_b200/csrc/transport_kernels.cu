@@ -3,6 +3,9 @@
 // the product path) and once with -DVMC_REAL=double --fmad=false (parity mode;
 // no contraction, like the reference built with -ffp-contract=off).
 #include "transport.cuh"
+#if VMC_REAL_IS_FLOAT
+#include "flight.cuh"
+#endif
 
 #ifndef VMC_REAL
 #define VMC_REAL float
@@ -57,5 +60,30 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
   }
 }
 
+#if VMC_REAL_IS_FLOAT
+// K1f (flight.cuh): the FP32 product kernel. Same register cap as K1.
+template <bool G, bool D, bool T, bool U>
+__global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const __grid_constant__ KernelArgs A) {
+  flight_body<G, D, T, U>(A);
+}
+
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform) {
+  const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
+#define VMC_FK(k, U)                                                                     \
+  case k:                                                                                \
+    return reinterpret_cast<const void*>(&k_flight<(k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);
+  if (uniform) {
+    switch (key) {
+      VMC_FK(0, true) VMC_FK(1, true) VMC_FK(2, true) VMC_FK(3, true)
+      VMC_FK(4, true) VMC_FK(5, true) VMC_FK(6, true) default: return reinterpret_cast<const void*>(&k_flight<true, true, true, true>);
+    }
+  }
+  switch (key) {
+    VMC_FK(0, false) VMC_FK(1, false) VMC_FK(2, false) VMC_FK(3, false)
+    VMC_FK(4, false) VMC_FK(5, false) VMC_FK(6, false) default: return reinterpret_cast<const void*>(&k_flight<true, true, true, false>);
+  }
+#undef VMC_FK
+}
+#endif
 
 }  // namespace vmc

@@ -30,7 +30,8 @@ from .errors import (AlreadyNormalized, DimensionMismatch, NonPositiveSlope, Sou
 from .scene import Marshalled, Scene, SimulationConfig, VoxelGrid
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvoxmc_b200.so")
+# VMC_LIB_PATH: load an alternative build of the same library (kernel A/B runs)
+LIB_PATH = os.environ.get("VMC_LIB_PATH") or os.path.join(_HERE, "lib", "libvoxmc_b200.so")
 _lib: Optional[C.CDLL] = None
 
 
