@@ -241,6 +241,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             raw = torch.empty(max(1, ecfg.det_capacity) * plan.rec_bytes, dtype=torch.uint8, pin_memory=True)
             pinned_det = raw.numpy().view(v.runtime._abi.det_record_dtype(plan.nmedia))
         times = []
+        eclocks = ClockSampler(local_rank)
+        eclocks.__enter__()
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             if world > 1:
@@ -254,6 +256,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             t1 = time.perf_counter()
             if i > 0:
                 times.append(t1 - t0)
+            if os.environ.get("BENCH_DEBUG"):
+                print(f"[bench] e2e call {i}: {(t1 - t0) * 1e3:.2f} ms", file=sys.stderr, flush=True)
+        eclocks.__exit__()
         tt = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -265,7 +270,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         else:
             d2h = plan.ncells * 8 + 4 * 8  # merged map + dispositions on rank 0
         e2e = {"value": total / (float(tt[0]) * 1e3), "unit": "photons/ms", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h),
+               "d2h_bytes_per_step": int(d2h), "clocks": eclocks.summary(),
                "path": ("run_group_dynamic -> vmc_run_range (scene upload, kernel, map + records download into pinned "
                         "host buffers), wall clock" if world == 1 else
                         "distributed.run_group_distributed per rank (scene upload, kernel, NCCL reduce, merged map "
@@ -283,7 +288,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     achieved = FLOP_PER_PHOTON[args.workload] * mine / (kern_ms_per * 1e-3) / 1e12
     roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
             "frac": achieved / fp32_peak, "traffic": None,
-            "kernel": "k_transport<float>", "kernel_ms": kern_ms_per,
+            "kernel": ("k_transport<float>" if os.environ.get("VMC_KERNEL") == "step" else "k_flight<float>"), "kernel_ms": kern_ms_per,
             "flop_per_photon": FLOP_PER_PHOTON[args.workload],
             "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 x {max_mhz:.0f} MHz (SIMT FP32; neither HBM nor tensor bound)",
             "l2_atomics_per_s": ATOMICS_PER_PHOTON[args.workload] * mine / (kern_ms_per * 1e-3)}

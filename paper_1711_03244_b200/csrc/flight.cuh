@@ -108,7 +108,10 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   int sx = 0, sy = 0, sz = 0;  // +-1, +-nx, +-nx*ny (direction of travel)
   int lab = 0, fax = 0;
   int gate = 0;
-  unsigned long long* gmap = reinterpret_cast<unsigned long long*>(A.cells);  // cells of `gate`
+  // this CTA's replica of the fluence map (see KernelArgs::rep_mask)
+  unsigned long long* const cbase =
+      reinterpret_cast<unsigned long long*>(A.cells) + (blockIdx.x & A.rep_mask) * A.rep_stride;
+  unsigned long long* gmap = cbase;  // cells of `gate`
   float fmua = 0, fns = 0;  // current medium (multi-label volumes): mua, n / c
   float sct = 0, sst = 0;  // scatter: cos/sin theta kept across azimuth retries
   uint32_t steps = 0, nscat = 0;
@@ -177,7 +180,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       const int g = gate_of(tt);
       if (g != gate) {
         gate = g;
-        gmap = reinterpret_cast<unsigned long long*>(A.cells) + static_cast<long long>(g) * A.nvox;
+        gmap = cbase + static_cast<long long>(g) * A.nvox;
       }
     }
   };
@@ -233,14 +236,17 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     const float rem = tmax - tf;
     const float dh = fmaxf(0.0f, rem * M.mm_per_ns);
     L = ds * M.ns_per_mm >= rem ? -dh : ds;  // horizon (transport.cpp:173-175) marked by the sign
-    phase = WALK;
+    // a flight that ends before the first face skips the walk (short flights:
+    // most of them in the head phantom's white matter)
+    phase = fminf(tmx, fminf(tmy, tmz)) >= fabsf(L) ? ENDF : WALK;
   };
 
   // ---- the flight ended inside the current voxel (ENDF, event phase):
-  // scattering point or horizon; absorb() already ran in the walk ----
+  // scattering point or horizon ----
   auto end_flight = [&]() {
     if constexpr (kTrace) ++steps;
     const float Ls = fabsf(L);
+    absorb(Ls);
     px += dx * Ls;
     py += dy * Ls;
     pz += dz * Ls;
@@ -268,12 +274,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   auto walk = [&]() {
     const float s = fminf(tmx, fminf(tmy, tmz));
     const float Ls = fabsf(L);
-    const bool end = s >= Ls;  // scatter / horizon win ties (transport.cpp:175, 191)
-    absorb(end ? Ls : s);
-    if (end) {
+    if (s >= Ls) {  // scatter / horizon win ties (transport.cpp:175, 191)
       phase = ENDF;
       return;
     }
+    absorb(s);
     if constexpr (kTrace) ++steps;
     deposit_run();  // the voxel left behind
     const bool a0 = tmx == s;  // ties -> lower axis (boundary_distance)
@@ -317,7 +322,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       if (M.iso) {
         ct = 2.0f * xi - 1.0f;
       } else {
-        const float f = __fdividef(M.hg_c, M.hg_d + M.hg_e * xi);
+        const float f = M.hg_c * Tr::rcp(M.hg_d + M.hg_e * xi);
         ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
       }
       sct = ct;
@@ -331,8 +336,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 #pragma unroll
     for (int k = 0; k < VMC_AZ_UNROLL; ++k) {
       if (k == 0 || !ok) {
-        ax_ = 2.0f * rng.template unit<float>() - 1.0f;
-        ay_ = 2.0f * rng.template unit<float>() - 1.0f;
+        ax_ = fmaf(rng.u24(), 0x1p-23f, -1.0f);  // 2u - 1, exact
+        ay_ = fmaf(rng.u24(), 0x1p-23f, -1.0f);
         r2 = ax_ * ax_ + ay_ * ay_;
         ok = r2 > 1e-12f && r2 <= 1.0f;
       }
@@ -557,7 +562,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     rs = scat_len();
     if constexpr (kGates) {
       gate = 0;
-      gmap = reinterpret_cast<unsigned long long*>(A.cells);
+      gmap = cbase;
     }
     if constexpr (kTrace) {
       steps = nscat = 0;

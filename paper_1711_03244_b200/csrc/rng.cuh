@@ -46,6 +46,10 @@ struct Xs128p {
 
   template <typename Real>
   __device__ __forceinline__ Real unit();
+
+  // top 24 bits of the next u64 as a float in [0, 2^24): unit<float>() * 2^24,
+  // for callers that fold the 2^-24 scale into an FMA
+  __device__ __forceinline__ float u24() { return static_cast<float>(static_cast<uint32_t>(next() >> 40)); }
 };
 
 template <>

@@ -104,6 +104,10 @@ struct KernelArgs {
   float inv_nxf, inv_nxyf;
   int event_pct;
   int absorb_mode;  // K1f absorb(): max mua*h*sqrt(3) < 0.012 -> 0, < 0.15 -> 1, else 2
+  // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
+  // (the host folds the replicas into the caller's map after the launch)
+  long long rep_stride;
+  int rep_mask, pad6;
 };
 
 // ---------------------------------------------------------------------------
@@ -240,10 +244,10 @@ __device__ __forceinline__ void transport_body(const KernelArgs& A) {
   };
 
   // one fixed-point add per deposit run (red.global.add.u64; the map is L2-resident)
+  unsigned long long* const cbase =
+      reinterpret_cast<unsigned long long*>(A.cells) + (blockIdx.x & A.rep_mask) * A.rep_stride;
   auto deposit = [&](int c, int gt, long long q) {
-    if (q != 0)
-      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (static_cast<long long>(c) + A.nvox * gt),
-                static_cast<unsigned long long>(q));
+    if (q != 0) atomicAdd(cbase + (static_cast<long long>(c) + A.nvox * gt), static_cast<unsigned long long>(q));
   };
   auto quant = [&](Real x) -> long long {
     if constexpr (kF32) {

@@ -33,7 +33,8 @@ def test_bench_single_gpu_line(gpu):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in REQUIRED:
         assert k in line, k
-    assert line["value"] > 0 and line["n_gpus"] == 1 and line["gpu_launches"] == 3
+    assert line["value"] > 0 and line["n_gpus"] == 1
+    assert line["gpu_launches"] >= 3 and line["gpu_launches"] % 3 == 0  # transport (+ replica fold) per step
     assert line["roofline"]["bound"] == "fp32" and 0 < line["roofline"]["frac"] < 1
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0

@@ -134,6 +134,21 @@ def test_determinism_and_range_split(gpu):
     assert tuple(int(x) for x in q) == a.totals_q
 
 
+@pytest.mark.parametrize("name", ["b1", "b3"])
+def test_map_replicas_bit_identical(gpu, monkeypatch, name):
+    """Fluence-map replicas (CTA b adds into copy b mod R, one fold kernel sums
+    them) change only where the integer adds land: maps, dispositions and
+    detector records are bit-identical for R = 1, 2, 8."""
+    st = setup(name, n=200_000)
+    runs = []
+    for r in ("1", "2", "8"):
+        monkeypatch.setenv("VMC_MAP_REPLICAS", r)
+        runs.append(gpu.run_group_dynamic(0, 200_000, 1, st.scene, st.config))
+    for x in runs[1:]:
+        assert np.array_equal(x.map.cells, runs[0].map.cells) and x.totals_q == runs[0].totals_q
+        assert x.det_count == runs[0].det_count
+
+
 def test_run_multi_single_device_equals_range(gpu):
     st = setup("b1", n=100_000)
     devs = [gpu.DeviceProfile(name="gpu0", cores=1, gpu=0)]

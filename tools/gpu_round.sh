@@ -9,7 +9,7 @@ timeout 400 python bench.py 2>&1 | tail -1 | tee gpurun_out/bench_$TAG.json
 timeout 400 python bench.py --impl reference --steps 2 --warmup 1 --cpu-seconds 6 2>&1 | tail -1 | tee gpurun_out/bench_ref_$TAG.json
 python tools/quick_tp.py 2>&1 | tee gpurun_out/tp_$TAG.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 --photons 10000000 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_transport -s 1 -c 1 -o gpurun_out/prof_b2_$TAG python tools/ncu_target.py b2 1e7 > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:k_(flight|transport)' -s 1 -c 1 -o gpurun_out/prof_b2_$TAG python tools/ncu_target.py b2 1e7 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -1 gpurun_out/ncu_full_$TAG.log
 cp paper_1711_03244_b200/lib/obj/transport_f32.o gpurun_out/transport_f32_$TAG.o
 for W in b1 b3 head; do
