@@ -271,13 +271,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // ---- one walk step of a lane in flight: the next face, or the end of the
   // flight. Branch-free apart from the rare interface / exit tail, so the
   // lanes of a warp stay converged ----
+  // A lane is WALK only while its next face comes before the end of the
+  // flight (checked at setup and after every face, scatter / horizon win ties,
+  // transport.cpp:175, 191), so every lane that enters a walk step crosses.
   auto walk = [&]() {
     const float s = fminf(tmx, fminf(tmy, tmz));
-    const float Ls = fabsf(L);
-    if (s >= Ls) {  // scatter / horizon win ties (transport.cpp:175, 191)
-      phase = ENDF;
-      return;
-    }
     absorb(s);
     if constexpr (kTrace) ++steps;
     deposit_run();  // the voxel left behind
@@ -309,6 +307,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         L = s;
         fax = a0 ? 0 : (a1 ? 1 : 2);
       }
+    } else if (fminf(tmx, fminf(tmy, tmz)) >= fabsf(L)) {
+      phase = ENDF;  // the flight ends in this voxel
     }
   };
 
