@@ -613,8 +613,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // the live lanes are still walking; the others wait for the event phase
     const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
     if (exhausted && dead == 0xffffffffu) break;
-    const int live = exhausted ? 32 - __popc(dead) : 32;
-    const int keep = (live * (100 - A.event_pct)) / 100;
+    const int keep = exhausted ? ((32 - __popc(dead)) * (100 - A.event_pct)) / 100 : A.walk_keep;
     for (;;) {
       const unsigned walking = __ballot_sync(0xffffffffu, phase == WALK);
       if (__popc(walking) <= keep) break;

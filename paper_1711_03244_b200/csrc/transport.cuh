@@ -107,7 +107,8 @@ struct KernelArgs {
   // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
   // (the host folds the replicas into the caller's map after the launch)
   long long rep_stride;
-  int rep_mask, pad6;
+  int rep_mask;
+  int walk_keep;  // K1f: a full warp walks while more than (32 * (100 - event_pct)) / 100 lanes walk
 };
 
 // ---------------------------------------------------------------------------

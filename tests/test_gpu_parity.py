@@ -69,6 +69,16 @@ def test_fp32_per_photon(gpu, ref, name, thr):
     assert np.abs(books - 1.0).max() < 1e-5
 
 
+def test_step_kernel_fp32_still_matches(gpu, ref, monkeypatch):
+    """The per-step FP32 kernel K1 (VMC_KERNEL=step, kept as the A/B baseline of
+    K1f) still follows the reference photon by photon."""
+    monkeypatch.setenv("VMC_KERNEL", "step")
+    st = setup("b2")
+    tr = gpu.trace_photons(st.scene, st.config, 0, 20_000)
+    rt = ref.walk(st.scene, st.config, 0, 20_000, threads=8, cells=False, traces=True)["traces"]
+    assert (tr["draws"] == rt["draws"]).mean() >= 0.995
+
+
 @pytest.mark.parametrize("name,tol", [("b1", 2e-4), ("b2", 2e-4), ("b3", 5e-4), ("head64", 5e-4)])
 def test_run_parity(gpu, ref, golden, name, tol):
     st = setup(name)
