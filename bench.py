@@ -300,6 +300,21 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                                  "unit": "GB/s", "frac": alg_bytes / (kern_ms_per * 1e-3) / 1e9 / hbm_peak,
                                  "algorithmic_bytes": alg_bytes,
                                  "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}}
+    # secondary: L2 atomics. Deposits per second (SURVEY §8(d) runs/photon) against the
+    # measured red.global.add.u64 rate of the B1 deposit-address distribution into 8
+    # replicas (tools/atomics_roofline.py; uniform addresses for the head map)
+    aprof = os.path.join(ROOT, "profiles", "r1_atomics_roofline.json")
+    if os.path.exists(aprof):
+        try:
+            with open(aprof) as f:
+                aj = json.load(f)
+            key = "uniform" if args.workload == "head" else "replay_rep8"
+            rate = roof["l2_atomics_per_s"]
+            roof["secondary"]["l2_atomics"] = {
+                "achieved": rate, "peak": aj[key], "unit": "red.add.u64/s", "frac": rate / aj[key],
+                "peak_basis": f"profiles/r1_atomics_roofline.json[{key}] (lib/atomics_bench, same B200 model)"}
+        except Exception:
+            pass
     prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(prof):
         try:
