@@ -289,9 +289,11 @@ struct vmc_plan {
   int grid = 0, grid_trace = 0;
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
-  // fluence-map replicas (small maps only): nrep copies the transport kernel
-  // deposits into, folded into the caller's map after each launch
+  // fluence-map scratch: nrep replicas (nrep > 1 for small maps) the transport
+  // kernel deposits into, folded into the caller's map after each launch. K1f
+  // always deposits into the scratch: the fold also books the deposited channel
   int nrep = 1;
+  bool scratch = false, fold_books_deposited = false;
   DevBuf rep;
 };
 
@@ -467,19 +469,36 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     int p2 = 1;
     while (p2 * 2 <= std::max(1, r)) p2 *= 2;
     P->nrep = p2;
-    if (P->nrep > 1) get(P->rep, cache ? &cache->rep : nullptr, static_cast<size_t>(P->nrep) * map_bytes);
+    P->fold_books_deposited = !f64 && !step_kernel;  // K1f keeps no deposited accumulator
+    P->scratch = P->nrep > 1 || P->fold_books_deposited;
+    if (P->scratch) get(P->rep, cache ? &cache->rep : nullptr, static_cast<size_t>(P->nrep) * map_bytes);
     A.rep_mask = P->nrep - 1;
     A.rep_stride = static_cast<long long>(P->ncells);
   }
 }
 
+// cells (+)= sum of the nrep scratch replicas; with `book`, the sum of every
+// added quantum goes to totals[0] (the deposited channel, exact in integers)
 __global__ void k_fold_replicas(unsigned long long* __restrict__ cells, const unsigned long long* __restrict__ rep,
-                                int nrep, uint64_t ncells) {
+                                int nrep, uint64_t ncells, int overwrite, unsigned long long* totals, int book) {
+  unsigned long long part = 0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < ncells;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     unsigned long long acc = 0;
-    for (int r = 0; r < nrep; ++r) acc += rep[static_cast<uint64_t>(r) * ncells + i];
-    cells[i] += acc;
+    for (int r = 0; r < nrep; ++r) acc += __ldcs(rep + static_cast<uint64_t>(r) * ncells + i);
+    cells[i] = overwrite ? acc : cells[i] + acc;
+    part += acc;
+  }
+  if (!book) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  __shared__ unsigned long long warp_sum[32];
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += warp_sum[w];
+    if (t) atomicAdd(totals, t);
   }
 }
 
@@ -491,8 +510,10 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   if (P->cfg.ndet > 0 && !d_det_count) fail_validation("detector count buffer is required");
   if (first + count < first) fail_validation("photon range overflows");
   ck(cudaSetDevice(P->device), "cudaSetDevice");
-  if (flags & VMC_RUN_ZERO) {
-    ck(cudaMemsetAsync(d_cells, 0, P->ncells * sizeof(int64_t), st), "zero cells");
+  const bool zero = (flags & VMC_RUN_ZERO) != 0;
+  if (zero) {
+    // with a scratch map the fold overwrites the caller's cells instead
+    if (!P->scratch || count == 0) ck(cudaMemsetAsync(d_cells, 0, P->ncells * sizeof(int64_t), st), "zero cells");
     ck(cudaMemsetAsync(d_totals, 0, 4 * sizeof(int64_t), st), "zero totals");
     if (d_det_count) ck(cudaMemsetAsync(d_det_count, 0, sizeof(uint64_t), st), "zero det count");
   }
@@ -502,7 +523,7 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   A.first = first;
   A.count = count;
   A.cells = reinterpret_cast<long long*>(d_cells);
-  if (P->nrep > 1) {
+  if (P->scratch) {
     ck(cudaMemsetAsync(P->rep.p, 0, static_cast<size_t>(P->nrep) * P->ncells * sizeof(int64_t), st), "zero replicas");
     A.cells = static_cast<long long*>(P->rep.p);
   }
@@ -518,10 +539,12 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv,
                       trace ? P->smem_trace : P->smem, st),
      "launch transport");
-  if (P->nrep > 1) {
+  if (P->scratch) {
     const int fb = static_cast<int>(std::min<uint64_t>((P->ncells + 255) / 256, static_cast<uint64_t>(P->sms) * 8));
     k_fold_replicas<<<fb, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_cells),
-                                        static_cast<const unsigned long long*>(P->rep.p), P->nrep, P->ncells);
+                                        static_cast<const unsigned long long*>(P->rep.p), P->nrep, P->ncells,
+                                        zero ? 1 : 0, reinterpret_cast<unsigned long long*>(d_totals),
+                                        P->fold_books_deposited ? 1 : 0);
     ck(cudaGetLastError(), "fold replicas");
   }
 }
@@ -1182,7 +1205,7 @@ uint64_t vmc_fnv1a64(const void* data, size_t bytes) {
 
 int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags) {
   (void)flags;
-  return plan ? 1 + (plan->nrep > 1 ? 1 : 0) : 0;  // transport (+ replica fold)
+  return plan ? 1 + (plan->scratch ? 1 : 0) : 0;  // transport (+ replica fold)
 }
 
 }  // extern "C"

@@ -87,7 +87,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   const int lane = threadIdx.x & 31;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
-  long long acc_dep = 0, acc_esc = 0, acc_kill = 0, acc_trunc = 0;
+  // escaped / killed / truncated quanta; the deposited channel is the sum of
+  // the map cells this launch added, computed by the fold kernel after it
+  long long acc_esc = 0, acc_kill = 0, acc_trunc = 0;
 
   int phase = DEAD;
   bool exhausted = false;
@@ -171,7 +173,6 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     const float dw = run_w0 - w;
     const long long q = quant(dw);
     atomicAdd(gmap + (vx + vy + vz), static_cast<unsigned long long>(q));  // q == 0 only if mua == 0
-    acc_dep += q;
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
   };
@@ -628,7 +629,6 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // ---- epilogue: dispositions (warp reduce) ----
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    acc_dep += __shfl_xor_sync(0xffffffffu, acc_dep, o);
     acc_esc += __shfl_xor_sync(0xffffffffu, acc_esc, o);
     acc_kill += __shfl_xor_sync(0xffffffffu, acc_kill, o);
     acc_trunc += __shfl_xor_sync(0xffffffffu, acc_trunc, o);
@@ -654,7 +654,6 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 #endif
   if (lane == 0) {
     unsigned long long* tot = reinterpret_cast<unsigned long long*>(A.totals);
-    if (acc_dep) atomicAdd(tot + 0, static_cast<unsigned long long>(acc_dep));
     if (acc_esc) atomicAdd(tot + 1, static_cast<unsigned long long>(acc_esc));
     if (acc_kill) atomicAdd(tot + 2, static_cast<unsigned long long>(acc_kill));
     if (acc_trunc) atomicAdd(tot + 3, static_cast<unsigned long long>(acc_trunc));
