@@ -474,6 +474,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     if (P->scratch) get(P->rep, cache ? &cache->rep : nullptr, static_cast<size_t>(P->nrep) * map_bytes);
     A.rep_mask = P->nrep - 1;
     A.rep_stride = static_cast<long long>(P->ncells);
+    if (static_cast<uint64_t>(P->nrep - 1) * P->ncells >= (1ull << 31)) fail_runtime("replica offsets overflow");
   }
 }
 

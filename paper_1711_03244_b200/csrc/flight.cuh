@@ -110,10 +110,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   int sx = 0, sy = 0, sz = 0;  // +-1, +-nx, +-nx*ny (direction of travel)
   int lab = 0, fax = 0;
   int gate = 0;
-  // this CTA's replica of the fluence map (see KernelArgs::rep_mask)
-  unsigned long long* const cbase =
-      reinterpret_cast<unsigned long long*>(A.cells) + (blockIdx.x & A.rep_mask) * A.rep_stride;
-  unsigned long long* gmap = cbase;  // cells of `gate`
+  // this CTA's replica of the fluence map (see KernelArgs::rep_mask); the host
+  // keeps rep_mask * rep_stride < 2^31, so the offset is a 32-bit cell index
+  const int roff = (static_cast<int>(blockIdx.x) & A.rep_mask) * static_cast<int>(A.rep_stride);
+  unsigned long long* const cbase = reinterpret_cast<unsigned long long*>(A.cells) + roff;
+  unsigned long long* gmap = cbase;  // cells of `gate` (gated launches)
   float fmua = 0, fns = 0;  // current medium (multi-label volumes): mua, n / c
   float sct = 0, sst = 0;  // scatter: cos/sin theta kept across azimuth retries
   uint32_t steps = 0, nscat = 0;
@@ -172,7 +173,14 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   auto deposit_run = [&]() {
     const float dw = run_w0 - w;
     const long long q = quant(dw);
-    atomicAdd(gmap + (vx + vy + vz), static_cast<unsigned long long>(q));  // q == 0 only if mua == 0
+    // q == 0 only if mua == 0; ungated launches index from the parameter-bank
+    // base (one IMAD.WIDE), gated ones from the gate's pointer
+    if constexpr (kGates) {
+      atomicAdd(gmap + (vx + vy + vz), static_cast<unsigned long long>(q));
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + vx + vy + vz),
+                static_cast<unsigned long long>(q));
+    }
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
   };
