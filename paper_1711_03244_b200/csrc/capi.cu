@@ -441,6 +441,9 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   // media table, plus per-thread per-label path lengths in detector mode
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
             (det ? static_cast<size_t>(vmc::kMaxDetMedia) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float)) : 0);
+  // K1f: escaped / killed / truncated quanta per thread after the above
+  A.acc_off = static_cast<int>((P->smem + 15) & ~static_cast<size_t>(15));
+  P->smem = static_cast<size_t>(A.acc_off) + 3 * vmc::kBlock * sizeof(long long);
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");

@@ -89,7 +89,10 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 
   // escaped / killed / truncated quanta; the deposited channel is the sum of
   // the map cells this launch added, computed by the fold kernel after it
-  long long acc_esc = 0, acc_kill = 0, acc_trunc = 0;
+  // they change once per photon, so they live in this thread's shared-memory
+  // slots (acc_sm[k * kBlock]: 0 escaped, 1 killed, 2 truncated), not in registers
+  long long* const acc_sm = reinterpret_cast<long long*>(smem + A.acc_off) + threadIdx.x;
+  acc_sm[0] = acc_sm[kBlock] = acc_sm[2 * kBlock] = 0;
 
   int phase = DEAD;
   bool exhausted = false;
@@ -263,7 +266,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     add_path(Ls);
     if (__float_as_int(L) < 0) {  // StepKind::Terminated (transport.cpp:181-187, 330-332)
       deposit_run();
-      acc_trunc += quant(w);
+      acc_sm[2 * kBlock] += quant(w);
       if constexpr (kTrace) pd_trunc += w;
       finish(2);
       return;
@@ -308,7 +311,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
     if (ev) {
       if (!kDet && ext && !A.reflect) {  // TerminateAtBoundary: ExitedDomain at once
-        acc_esc += quant(w);
+        acc_sm[0] += quant(w);
         if constexpr (kTrace) pd_esc += w;
         finish(0);
       } else {
@@ -389,12 +392,12 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       const long long qb = quant(w);
       if constexpr (kTrace) pd_kill += w;
       if (!survive) {
-        acc_kill += qb;
+        acc_sm[kBlock] += qb;
         finish(1);
         return;
       }
       w *= A.rmultf;
-      acc_kill += qb - quant(w);
+      acc_sm[kBlock] += qb - quant(w);
       if constexpr (kTrace) pd_kill -= w;
       run_w0 = w;
     }
@@ -460,7 +463,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       }
     }
     if (exited) {  // ExitedDomain: escaped += w (transport.cpp:348-350)
-      acc_esc += quant(w);
+      acc_sm[0] += quant(w);
       if constexpr (kTrace) pd_esc += w;
       if constexpr (kDet) {
         int hit = -1;
@@ -635,6 +638,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   }
 
   // ---- epilogue: dispositions (warp reduce) ----
+  long long acc_esc = acc_sm[0], acc_kill = acc_sm[kBlock], acc_trunc = acc_sm[2 * kBlock];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     acc_esc += __shfl_xor_sync(0xffffffffu, acc_esc, o);

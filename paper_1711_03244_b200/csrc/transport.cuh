@@ -109,6 +109,8 @@ struct KernelArgs {
   long long rep_stride;
   int rep_mask;
   int walk_keep;  // K1f: a full warp walks while more than (32 * (100 - event_pct)) / 100 lanes walk
+  int acc_off;    // K1f: byte offset of the per-thread disposition accumulators in shared memory
+  int pad7;
 };
 
 // ---------------------------------------------------------------------------
