@@ -398,6 +398,10 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   A.rec_stride = static_cast<int>(P->rec_stride);
   for (int k = 0; k < c->ndet; ++k)
     for (int j = 0; j < 4; ++j) A.det[k][j] = c->det[4 * k + j];
+  for (int k = 0; k < c->ndet; ++k) {
+    for (int j = 0; j < 3; ++j) A.detf[k][j] = static_cast<float>(c->det[4 * k + j]);
+    A.detf[k][3] = static_cast<float>(c->det[4 * k + 3] * c->det[4 * k + 3]);
+  }
   A.det_cap = c->det_capacity;
 
   const bool gates = c->ngates > 1, det = c->ndet > 0;

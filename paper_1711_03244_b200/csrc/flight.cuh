@@ -437,14 +437,16 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         const float n1 = M.n, n2 = sm_media[nl].n;
         const float ci = fabsf(dax);
         const float si2 = fmaxf(0.0f, 1.0f - ci * ci);
-        const float eta = n1 / n2;
+        // MUFU reciprocal / sqrt: R only meets a 24-bit uniform, and the
+        // interface code runs on few lanes at a time, so its length is its cost
+        const float eta = n1 * Tr::rcp(n2);
         const float st2 = eta * eta * si2;
         if (st2 > 1.0f) {
           back = true;  // total internal reflection: deterministic flip
         } else {
-          const float cost = sqrtf(1.0f - st2);
-          const float rsp = (n1 * ci - n2 * cost) / (n1 * ci + n2 * cost);
-          const float rpp = (n1 * cost - n2 * ci) / (n1 * cost + n2 * ci);
+          const float cost = Tr::sqrt_(1.0f - st2);
+          const float rsp = (n1 * ci - n2 * cost) * Tr::rcp(n1 * ci + n2 * cost);
+          const float rpp = (n1 * cost - n2 * ci) * Tr::rcp(n1 * cost + n2 * ci);
           const float R = 0.5f * (rsp * rsp + rpp * rpp);
           if (rng.template unit<float>() < R) {
             back = true;
@@ -468,10 +470,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       if constexpr (kDet) {
         int hit = -1;
         for (int k = 0; k < A.ndet; ++k) {
-          const double ex = static_cast<double>(px) - A.det[k][0];
-          const double ey = static_cast<double>(py) - A.det[k][1];
-          const double ez = static_cast<double>(pz) - A.det[k][2];
-          if (ex * ex + ey * ey + ez * ez <= A.det[k][3] * A.det[k][3]) {
+          // FP32 like the exit position itself (detf = {x, y, z, r^2})
+          const float ex = px - A.detf[k][0], ey = py - A.detf[k][1], ez = pz - A.detf[k][2];
+          if (ex * ex + ey * ey + ez * ez <= A.detf[k][3]) {
             hit = k;
             break;
           }

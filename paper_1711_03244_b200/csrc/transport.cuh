@@ -111,6 +111,7 @@ struct KernelArgs {
   int walk_keep;  // K1f: a full warp walks while more than (32 * (100 - event_pct)) / 100 lanes walk
   int acc_off;    // K1f: byte offset of the per-thread disposition accumulators in shared memory
   int pad7;
+  float detf[kMaxDet][4];  // K1f: detector disks as {x, y, z, r^2} in FP32
 };
 
 // ---------------------------------------------------------------------------
