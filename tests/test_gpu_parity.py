@@ -305,11 +305,35 @@ def _corner_scene(kind):
     elif kind == "oblique":  # oblique pencil off a voxel corner
         media = [air, v.OpticalProperties(0.01, 1.0, 0.9, 1.37)]
         src = v.Source((7.0, 9.0, 0.0), (0.3, -0.2, 0.9))
+    elif kind == "ballistic":  # mus = 0 shell + in-grid air (label 0): long flights, same-n label changes
+        media = [air, v.OpticalProperties(0.02, 2.0, 0.8, 1.37), v.OpticalProperties(0.004, 0.0, 0.0, 1.37)]
+        lab[(r2 > 16) & (r2 <= 49)] = 2
+        lab[:, :, n - 3:] = 0
+    elif kind == "aniso_grid":  # non-cubic grid, non-integer voxel size (scaled-index decode, plane landing)
+        nx, ny, nz = 17, 23, 29
+        lab = np.ones((nz, ny, nx), np.uint8)
+        media = [air, v.OpticalProperties(0.01, 1.5, 0.85, 1.4)]
+        grid = v.VoxelGrid((nx, ny, nz), 0.37, lab, media)
+        src = v.Source((17 * 0.37 / 2, 23 * 0.37 / 2, 0.0), (0.1, 0.05, 1.0))
+        return v.Scene(grid, src), cfg
     grid = v.VoxelGrid((n, n, n), 1.0, lab, media)
     return v.Scene(grid, src), cfg
 
 
-CORNERS = ["roulette", "horizon", "backward", "dense_inclusion", "terminate_inner", "oblique"]
+CORNERS = ["roulette", "horizon", "backward", "dense_inclusion", "terminate_inner", "oblique", "ballistic",
+           "aniso_grid"]
+
+
+@pytest.mark.parametrize("kind", CORNERS)
+def test_corner_fp32_per_photon(gpu, ref, kind):
+    """K1f (flight kernel) photon by photon on the corner scenes: same RNG draw
+    counts as the FP64 reference for nearly all photons, exact weight books."""
+    scene, cfg = _corner_scene(kind)
+    tr = gpu.trace_photons(scene, cfg, 0, 5000)
+    rt = ref.walk(scene, cfg, 0, 5000, threads=8, cells=False, traces=True)["traces"]
+    assert (tr["draws"] == rt["draws"]).mean() >= 0.97
+    books = tr["deposited"] + tr["escaped"] + tr["killed"] + tr["truncated"]
+    assert np.abs(books - 1.0).max() < 1e-5
 
 
 @pytest.mark.parametrize("kind", CORNERS)
