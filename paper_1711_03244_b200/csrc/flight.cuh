@@ -17,24 +17,33 @@
 //                  L = min(remaining_scat / mus, horizon distance)
 //                  (horizon iff d_scatter * n/c >= tmax - t, :169-175), the
 //                  signed cell strides of the three axes;
-//   crossing loop  per voxel face (the common, cheap event): s = min(tm);
-//                  s >= L ends the flight inside the voxel (scatter ties win,
-//                  :191); otherwise the segment's absorbed weight
-//                  w (1 - exp(-mua ds)) closes the voxel's run with one
-//                  fixed-point red.add for the voxel left behind (deposit into
-//                  the pre-step voxel, :323-327), step the voxel index, exterior
-//                  test on the moved axis, and (multi-label volumes) the
-//                  neighbour label — a label change ends the flight at the face
-//                  (interface, :214-223);
-//   event phase    scatter (hg_scatter + new free path + roulette, :126-147,
-//                  :333-343), interface (handle_interface, :227-298), horizon,
-//                  exit, refill — run by the warp once enough lanes wait for one.
+//   walk step      per voxel face (the common, cheap event). A lane walks only
+//                  while its next face s = min(tm) comes before L (checked at
+//                  setup and after every face; scatter / horizon win ties,
+//                  :175,191), so every lane in a walk step crosses: the
+//                  segment's absorbed weight w (1 - exp(-mua ds)) closes the
+//                  voxel's deposit run with one fixed-point red.add (deposit
+//                  into the pre-step voxel, :323-327), the voxel index steps,
+//                  the moved axis is tested against the exterior and
+//                  (multi-label volumes) the neighbour label is read — a label
+//                  change ends the flight at the face (interface, :214-223);
+//   event phase    end of flight, scatter (hg_scatter + new free path +
+//                  roulette, :126-147, :333-343), interface (handle_interface,
+//                  :227-298), horizon, exit, refill, next flight's setup — run
+//                  by the warp once >= event_pct % of its live lanes wait for one.
 //
-// A crossing costs ~35 SASS instructions instead of a full advance() step, and
+// A face costs ~40 SASS instructions instead of a full advance() step, and
 // the expensive scatter/interface code runs on mostly full warps. Floating
 // point differs from the step kernel only at the ulp level (face distances
 // accumulated from the flight start instead of recomputed per face), which moves no
 // discrete decision beyond the per-photon draw-count gates of the parity tests.
+//
+// Deposits go into one of KernelArgs::rep_mask + 1 replicas of the map (CTA
+// index mod replicas): the voxels next to the source take every photon's
+// first deposits, and spreading them over replicas keeps the same-address
+// L2 red.add rate off the critical path. The host folds the replicas into the
+// caller's map and books the deposited channel as the exact sum of the quanta
+// it adds, so the kernel keeps no deposited accumulator.
 //
 // Voxel coordinates are kept pre-scaled (vx, vy*nx, vz*nx*ny) so the cell
 // index is one add; the unscaled y/z coordinates are decoded (exact float
@@ -87,10 +96,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   const int lane = threadIdx.x & 31;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
-  // escaped / killed / truncated quanta; the deposited channel is the sum of
-  // the map cells this launch added, computed by the fold kernel after it
-  // they change once per photon, so they live in this thread's shared-memory
-  // slots (acc_sm[k * kBlock]: 0 escaped, 1 killed, 2 truncated), not in registers
+  // escaped / killed / truncated quanta change once per photon, so they live in
+  // this thread's shared-memory slots (acc_sm[k * kBlock]: 0 escaped, 1 killed,
+  // 2 truncated), not in registers; the deposited channel is booked by the fold
   long long* const acc_sm = reinterpret_cast<long long*>(smem + A.acc_off) + threadIdx.x;
   acc_sm[0] = acc_sm[kBlock] = acc_sm[2 * kBlock] = 0;
 
