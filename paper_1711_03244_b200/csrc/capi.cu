@@ -418,8 +418,6 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
       uniform = false;
     }
   }
-  A.inv_nxf = 1.0f / static_cast<float>(s->nx);
-  A.inv_nxyf = 1.0f / static_cast<float>(A.nxy);
   // measured: 70-80 best; clamped so a warp always walks while >= 1 lane of 32 does
   A.event_pct = std::min(100, std::max(4, env_int("VMC_EVENT_PCT", 80)));
   A.walk_keep = (32 * (100 - A.event_pct)) / 100;

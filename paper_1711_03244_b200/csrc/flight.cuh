@@ -45,9 +45,8 @@
 // caller's map and books the deposited channel as the exact sum of the quanta
 // it adds, so the kernel keeps no deposited accumulator.
 //
-// Voxel coordinates are kept pre-scaled (vx, vy*nx, vz*nx*ny) so the cell
-// index is one add; the unscaled y/z coordinates are decoded (exact float
-// multiply-round) only at flight setup and on interfaces.
+// Voxel coordinates are kept as integers per axis; the linear cell index is
+// two IMADs (FMA pipe) where a deposit or label read needs it.
 #pragma once
 
 #include <cstdio>
@@ -88,8 +87,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   };
 
   const int nx = A.nx;
+  const int ny = A.ny, nz = A.nz;
   const int nxy = static_cast<int>(A.nxy);
-  const int nvox = static_cast<int>(A.nvox);
   const float h = A.hf;
   const float tmax = A.tmaxf;
   const float qscale = A.qscalef;
@@ -117,8 +116,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
                      // FACE: distance of the face event
   // incremental DDA
   float tmx = 0, tmy = 0, tmz = 0, tdx = 0, tdy = 0, tdz = 0;
-  int vx = 0, vy = 0, vz = 0;  // vx, vy * nx, vz * nx * ny
-  int sx = 0, sy = 0, sz = 0;  // +-1, +-nx, +-nx*ny (direction of travel)
+  int vx = 0, vy = 0, vz = 0;  // voxel coordinates
+  int sx = 0, sy = 0, sz = 0;  // +-1: direction of travel per axis
   int lab = 0, fax = 0;
   int gate = 0;
   // this CTA's replica of the fluence map (see KernelArgs::rep_mask); the host
@@ -176,9 +175,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     w = fmaf(-w, f, w);
     s0 = s;
   };
-  auto decode = [&](int scaled, float inv) -> int {  // exact: scaled is a multiple of the stride
-    return __float2int_rn(__int2float_rn(scaled) * inv);
-  };
+  auto cell = [&]() -> int { return vx + nx * vy + nxy * vz; };  // x-fastest linear index (two IMAD)
   // close the open deposit run at weight w_new: one fixed-point add into the
   // voxel the run belongs to (the map is L2-resident for cube60)
   auto deposit_run = [&]() {
@@ -187,9 +184,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // q == 0 only if mua == 0; ungated launches index from the parameter-bank
     // base (one IMAD.WIDE), gated ones from the gate's pointer
     if constexpr (kGates) {
-      atomicAdd(gmap + (vx + vy + vz), static_cast<unsigned long long>(q));
+      atomicAdd(gmap + cell(), static_cast<unsigned long long>(q));
     } else {
-      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + vx + vy + vz),
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + cell()),
                 static_cast<unsigned long long>(q));
     }
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
@@ -239,7 +236,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
     s0 = 0.0f;
     const float ix = Tr::rcp(dx), iy = Tr::rcp(dy), iz = Tr::rcp(dz);  // +-inf for 0
-    const int ux = vx, uy = decode(vy, A.inv_nxf), uz = decode(vz, A.inv_nxyf);
+    const int ux = vx, uy = vy, uz = vz;
     const float t0 = (static_cast<float>(ux + (dx > 0.0f ? 1 : 0)) * h - px) * ix;
     const float t1 = (static_cast<float>(uy + (dy > 0.0f ? 1 : 0)) * h - py) * iy;
     const float t2 = (static_cast<float>(uz + (dz > 0.0f ? 1 : 0)) * h - pz) * iz;
@@ -250,8 +247,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     tdy = h * fabsf(iy);
     tdz = h * fabsf(iz);
     sx = dx > 0.0f ? 1 : -1;
-    sy = dy > 0.0f ? nx : -nx;
-    sz = dz > 0.0f ? nxy : -nxy;
+    sy = dy > 0.0f ? 1 : -1;
+    sz = dz > 0.0f ? 1 : -1;
     const float ds = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
     const float rem = tmax - tf;
     const float dh = fmaxf(0.0f, rem * M.mm_per_ns);
@@ -310,12 +307,12 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if (a1) tmy += tdy;
     if (a2) tmz += tdz;
     const bool ext = static_cast<unsigned>(vx) >= static_cast<unsigned>(nx) ||
-                     static_cast<unsigned>(vy) >= static_cast<unsigned>(nxy) ||
-                     static_cast<unsigned>(vz) >= static_cast<unsigned>(nvox);
+                     static_cast<unsigned>(vy) >= static_cast<unsigned>(ny) ||
+                     static_cast<unsigned>(vz) >= static_cast<unsigned>(nz);
     if constexpr (kGates) set_gate(tf + s * nsmm_());
     bool ev = ext;
     if constexpr (!kUni) {
-      if (!ext) ev = static_cast<int>(__ldg(A.labels + (vx + vy + vz))) != lab;
+      if (!ext) ev = static_cast<int>(__ldg(A.labels + cell())) != lab;
     }
     if (ev) {
       if (!kDet && ext && !A.reflect) {  // TerminateAtBoundary: ExitedDomain at once
@@ -419,7 +416,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     {
       // land exactly on the crossed plane (transport.cpp:197-204); the voxel
       // index has already moved, so the plane is its near face
-      const int u = ax == 0 ? vx : (ax == 1 ? decode(vy, A.inv_nxf) : decode(vz, A.inv_nxyf));
+      const int u = ax == 0 ? vx : (ax == 1 ? vy : vz);
       const float dax = ax == 0 ? dx : (ax == 1 ? dy : dz);
       const float plane = static_cast<float>(dax > 0.0f ? u : u + 1) * h;
       px = ax == 0 ? plane : px + dx * s;
@@ -430,9 +427,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     const Medium<float>& M = medium(lab);
     rs = fmaxf(0.0f, rs - s * M.mus);
     const bool ext = static_cast<unsigned>(vx) >= static_cast<unsigned>(nx) ||
-                     static_cast<unsigned>(vy) >= static_cast<unsigned>(nxy) ||
-                     static_cast<unsigned>(vz) >= static_cast<unsigned>(nvox);
-    const int nl = ext ? 0 : static_cast<int>(__ldg(A.labels + (vx + vy + vz)));
+                     static_cast<unsigned>(vy) >= static_cast<unsigned>(ny) ||
+                     static_cast<unsigned>(vz) >= static_cast<unsigned>(nz);
+    const int nl = ext ? 0 : static_cast<int>(__ldg(A.labels + cell()));
     bool exited = false, back = false;
     if (ext && !A.reflect) {
       exited = true;  // TerminateAtBoundary (transport.cpp:234-237)
@@ -575,8 +572,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       lab = A.lab0;
     }
     vx = ux;
-    vy = uy * nx;
-    vz = uz * nxy;
+    vy = uy;
+    vz = uz;
     w = 1.0f;
     tf = 0.0f;
     run_w0 = 1.0f;

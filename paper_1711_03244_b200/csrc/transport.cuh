@@ -98,10 +98,9 @@ struct KernelArgs {
   // the parameter bank (constant operands, no shared-memory address math)
   Medium<float> uni_f;
   Medium<double> uni_d;
-  // K1f (flight.cuh): 1/nx and 1/(nx*ny) to decode the scaled voxel
-  // coordinates, and the event-phase trigger (percent of live lanes that
+  // K1f (flight.cuh): the event-phase trigger (percent of live lanes that
   // must have finished their flight before the warp runs the event phase)
-  float inv_nxf, inv_nxyf;
+  float pad8, pad9;
   int event_pct;
   int absorb_mode;  // K1f absorb(): max mua*h*sqrt(3) < 0.012 -> 0, < 0.15 -> 1, else 2
   // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
