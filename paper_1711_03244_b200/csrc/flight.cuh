@@ -529,9 +529,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   };
 
   // ---- launch (transport.cpp:83-106) ----
-  auto launch = [&](unsigned long long my) {
-    idx = A.first + my;
-    rng.seed(A.seed, idx);
+  // the caller has set idx and seeded rng (from the warp's seed stash)
+  auto launch = [&]() {
     int ux, uy, uz;
     if (A.iso_source) {
       const float ct = 2.0f * rng.template unit<float>() - 1.0f;
@@ -593,6 +592,19 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     phase = SETUP;
   };
 
+  // per-warp seed stash in shared memory: 32 seeded RNG states of the photons
+  // st_base + 0..31 and a header {next unused slot, valid slots}; st_base and
+  // st_claimed_all are warp-uniform registers
+  const int warp = threadIdx.x >> 5;
+  unsigned char* const stash = smem + A.stash_off + warp * (32 * 16 + 16);
+  uint64_t* const st_a = reinterpret_cast<uint64_t*>(stash);
+  uint64_t* const st_b = st_a + 32;
+  int* const st_hdr = reinterpret_cast<int*>(stash + 32 * 16);
+  if (lane == 0) st_hdr[0] = st_hdr[1] = 0;
+  __syncwarp();
+  unsigned long long st_base = 0;
+  bool st_claimed_all = false;
+
 #ifdef VMC_STATS
   unsigned long long st_[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #define VMC_ST(i, v) st_[i] += exhausted ? 0 : (v)  // steady state only (no drain tail)
@@ -611,14 +623,56 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 #endif
     {
       const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
-      if (dead && !exhausted) {  // refill: one claim per warp (GroupCounter::claim)
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(A.claim, static_cast<unsigned long long>(__popc(dead)));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base + __popc(dead) >= A.count) exhausted = true;
-        if (phase == DEAD) {
-          const unsigned long long my = base + __popc(dead & lanemask_lt);
-          if (my < A.count) launch(my);
+      if (dead && !exhausted) {
+        // Refill from the warp's seed stash: photons are claimed 32 at a time
+        // (GroupCounter::claim, one atomicAdd) and all 32 lanes seed them at once
+        // (two splitmix64 finalizers each, rng.cpp:5-19), so a relaunch no longer
+        // runs the seeding on the one or two lanes that happen to be free.
+        const int nd = __popc(dead);
+        const int rank = __popc(dead & lanemask_lt);
+        const int next = st_hdr[0], valid = st_hdr[1];
+        const int take1 = min(nd, valid - next);
+        int slot = -1;
+        unsigned long long pid = 0;
+        if (phase == DEAD && rank < take1) {
+          slot = next + rank;
+          pid = st_base + static_cast<unsigned long long>(slot);
+          rng.a = st_a[slot];
+          rng.b = st_b[slot];
+        }
+        int new_next = next + take1;
+        if (nd > take1 && !st_claimed_all) {  // claim and seed a new batch of 32
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(A.claim, 32ull);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          const int nvalid = base >= A.count ? 0 : static_cast<int>(min(32ull, A.count - base));
+          if (base + 32 >= A.count) st_claimed_all = true;
+          __syncwarp();
+          if (lane < nvalid) {
+            Rng sr;
+            sr.seed(A.seed, A.first + base + lane);
+            st_a[lane] = sr.a;
+            st_b[lane] = sr.b;
+          }
+          __syncwarp();
+          const int take2 = min(nd - take1, nvalid);
+          if (phase == DEAD && rank >= take1 && rank - take1 < take2) {
+            slot = rank - take1;
+            pid = base + static_cast<unsigned long long>(slot);
+            rng.a = st_a[slot];
+            rng.b = st_b[slot];
+          }
+          st_base = base;
+          new_next = take2;
+          if (lane == 0) st_hdr[1] = nvalid;
+        }
+        if (lane == 0) st_hdr[0] = new_next;
+        __syncwarp();
+        if (st_claimed_all && st_hdr[0] == st_hdr[1]) exhausted = true;
+        if (slot >= 0) {
+          idx = A.first + pid;
+          if constexpr (kTrace) rng.draws = 0;
+          launch();
         }
       }
     }
