@@ -448,7 +448,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   A.acc_off = static_cast<int>((P->smem + 15) & ~static_cast<size_t>(15));
   P->smem = static_cast<size_t>(A.acc_off) + 3 * vmc::kBlock * sizeof(long long);
   A.stash_off = static_cast<int>((P->smem + 15) & ~static_cast<size_t>(15));
-  P->smem = static_cast<size_t>(A.stash_off) + (vmc::kBlock / 32) * (32 * 16 + 16);
+  P->smem = static_cast<size_t>(A.stash_off) + (vmc::kBlock / 32) * (32 * 20 + 16);
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");

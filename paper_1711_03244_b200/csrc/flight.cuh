@@ -206,10 +206,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       if (lab >= 1) pp_sm[(lab - 1) * kBlock] += s;
     }
   };
-  auto scat_len = [&]() -> float {  // transport.cpp:14-17
-    const float u = rng.template unit<float>();
+  auto scat_len_of = [&](Rng& r) -> float {  // transport.cpp:14-17
+    const float u = r.template unit<float>();
     return -Tr::ln(u > 0.0f ? u : 0x1p-25f);
   };
+  auto scat_len = [&]() -> float { return scat_len_of(rng); };
   auto finish = [&](int kind) {  // 0 escaped 1 killed 2 truncated
     if constexpr (kTrace) {
       vmc_photon_trace tr;
@@ -576,7 +577,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     w = 1.0f;
     tf = 0.0f;
     run_w0 = 1.0f;
-    rs = scat_len();
+    if (A.iso_source) rs = scat_len();  // pencil: drawn in the seed batch
     if constexpr (kGates) {
       gate = 0;
       gmap = cbase;
@@ -596,10 +597,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // st_base + 0..31 and a header {next unused slot, valid slots}; st_base and
   // st_claimed_all are warp-uniform registers
   const int warp = threadIdx.x >> 5;
-  unsigned char* const stash = smem + A.stash_off + warp * (32 * 16 + 16);
+  unsigned char* const stash = smem + A.stash_off + warp * (32 * 20 + 16);
   uint64_t* const st_a = reinterpret_cast<uint64_t*>(stash);
   uint64_t* const st_b = st_a + 32;
-  int* const st_hdr = reinterpret_cast<int*>(stash + 32 * 16);
+  float* const st_rs = reinterpret_cast<float*>(stash + 32 * 16);  // pencil sources: first free path
+  int* const st_hdr = reinterpret_cast<int*>(stash + 32 * 16 + 32 * 4);
   if (lane == 0) st_hdr[0] = st_hdr[1] = 0;
   __syncwarp();
   unsigned long long st_base = 0;
@@ -639,6 +641,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
           pid = st_base + static_cast<unsigned long long>(slot);
           rng.a = st_a[slot];
           rng.b = st_b[slot];
+          rs = st_rs[slot];
         }
         int new_next = next + take1;
         if (nd > take1 && !st_claimed_all) {  // claim and seed a new batch of 32
@@ -651,6 +654,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
           if (lane < nvalid) {
             Rng sr;
             sr.seed(A.seed, A.first + base + lane);
+            if (!A.iso_source) st_rs[lane] = scat_len_of(sr);  // a pencil's first draw (transport.cpp:105)
             st_a[lane] = sr.a;
             st_b[lane] = sr.b;
           }
@@ -661,6 +665,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
             pid = base + static_cast<unsigned long long>(slot);
             rng.a = st_a[slot];
             rng.b = st_b[slot];
+            rs = st_rs[slot];
           }
           st_base = base;
           new_next = take2;
@@ -671,7 +676,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         if (st_claimed_all && st_hdr[0] == st_hdr[1]) exhausted = true;
         if (slot >= 0) {
           idx = A.first + pid;
-          if constexpr (kTrace) rng.draws = 0;
+          if constexpr (kTrace) rng.draws = A.iso_source ? 0 : 1;
           launch();
         }
       }
