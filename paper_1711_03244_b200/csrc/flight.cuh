@@ -62,7 +62,10 @@ __device__ unsigned long long vmc_flight_stats[12];
 __device__ unsigned int vmc_flight_done;
 #endif
 
-template <bool kGates, bool kDet, bool kTrace, bool kUni>
+// kAbs: -1 = absorb() picks its series per launch (KernelArgs::absorb_mode);
+// 0 = compiled for absorb_mode 0 (every mua * h * sqrt(3) < 0.012, the cube60
+// phantoms), which drops the warp-uniform mode test from the walk step
+template <bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Tr = RealTraits<float>;
   using Rng = Xs128p<kTrace>;
@@ -162,7 +165,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   auto absorb = [&](float s) {
     const float x = mua_() * (s - s0);
     float f;
-    if (A.absorb_mode == 0) {
+    if (kAbs == 0 || A.absorb_mode == 0) {
       f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f)));
     } else {
       f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f - x * (1.0f / 120.0f)))));

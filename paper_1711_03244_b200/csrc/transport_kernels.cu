@@ -62,13 +62,15 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
 
 #if VMC_REAL_IS_FLOAT
 // K1f (flight.cuh): the FP32 product kernel. Same register cap as K1.
-template <bool G, bool D, bool T, bool U>
+template <bool G, bool D, bool T, bool U, int Abs = -1>
 __global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const __grid_constant__ KernelArgs A) {
-  flight_body<G, D, T, U>(A);
+  flight_body<G, D, T, U, Abs>(A);
 }
 
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform) {
+// small_mua: the launch's absorb_mode is 0 (see flight_body's kAbs)
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, bool small_mua) {
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
+  if (uniform && small_mua && key == 0) return reinterpret_cast<const void*>(&k_flight<false, false, false, true, 0>);
 #define VMC_FK(k, U)                                                                     \
   case k:                                                                                \
     return reinterpret_cast<const void*>(&k_flight<(k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);
