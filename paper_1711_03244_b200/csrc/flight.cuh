@@ -693,7 +693,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // the live lanes are still walking; the others wait for the event phase
     const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
     if (exhausted && dead == 0xffffffffu) break;
-    const int keep = exhausted ? ((32 - __popc(dead)) * (100 - A.event_pct)) / 100 : A.walk_keep;
+    // walk_keep scaled to the live lanes (all 32 until the photons run out)
+    const int keep = ((32 - (exhausted ? __popc(dead) : 0)) * A.walk_keep) >> 5;
     for (;;) {
       const unsigned walking = __ballot_sync(0xffffffffu, phase == WALK);
       if (__popc(walking) <= keep) break;
