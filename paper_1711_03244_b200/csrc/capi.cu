@@ -33,7 +33,7 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, bool small_mua);
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode);
 }  // namespace vmc
 
 namespace {
@@ -438,8 +438,8 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     P->kern = vmc::transport_kernel_float(gates, det, false, uniform);
     P->kern_trace = vmc::transport_kernel_float(gates, det, true, uniform);
   } else {
-    P->kern = vmc::flight_kernel_float(gates, det, false, uniform, A.absorb_mode == 0);
-    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, A.absorb_mode == 0);
+    P->kern = vmc::flight_kernel_float(gates, det, false, uniform, A.absorb_mode);
+    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, A.absorb_mode);
   }
   // media table, plus per-thread per-label path lengths in detector mode
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +

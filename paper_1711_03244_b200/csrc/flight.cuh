@@ -63,8 +63,9 @@ __device__ unsigned int vmc_flight_done;
 #endif
 
 // kAbs: -1 = absorb() picks its series per launch (KernelArgs::absorb_mode);
-// 0 = compiled for absorb_mode 0 (every mua * h * sqrt(3) < 0.012, the cube60
-// phantoms), which drops the warp-uniform mode test from the walk step
+// 0 / 1 = compiled for absorb_mode 0 (every mua * h * sqrt(3) < 0.012, the
+// cube60 phantoms) / 1 (< 0.15, the head phantom), which drops the warp-uniform
+// mode tests from every absorb()
 template <bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Tr = RealTraits<float>;
@@ -165,11 +166,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   auto absorb = [&](float s) {
     const float x = mua_() * (s - s0);
     float f;
-    if (kAbs == 0 || A.absorb_mode == 0) {
+    if (kAbs == 0 || (kAbs < 0 && A.absorb_mode == 0)) {
       f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f)));
     } else {
       f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f - x * (1.0f / 120.0f)))));
-      if (A.absorb_mode == 2 && x >= 0.15f) {
+      if (kAbs < 0 && A.absorb_mode == 2 && x >= 0.15f) {
         float e;
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
         f = 1.0f - e;

@@ -67,10 +67,13 @@ __global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const _
   flight_body<G, D, T, U, Abs>(A);
 }
 
-// small_mua: the launch's absorb_mode is 0 (see flight_body's kAbs)
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, bool small_mua) {
+// absorb_mode: the launch's KernelArgs::absorb_mode; the BASELINE workloads'
+// production variants are compiled for their mode (see flight_body's kAbs)
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode) {
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
-  if (uniform && small_mua && key == 0) return reinterpret_cast<const void*>(&k_flight<false, false, false, true, 0>);
+  if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<false, false, false, true, 0>);
+  if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<false, true, false, false, 0>);
+  if (absorb_mode == 1 && !uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<true, false, false, false, 1>);
 #define VMC_FK(k, U)                                                                     \
   case k:                                                                                \
     return reinterpret_cast<const void*>(&k_flight<(k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);
