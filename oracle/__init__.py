@@ -216,6 +216,8 @@ class COracle(_Base):
         lib.orc_fresnel.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.orc_walk.argtypes = [P(_abi.vmc_scene), P(_abi.vmc_config), u64, u64, C.c_int, vp, vp,
                                  P(C.c_double), vp, P(u64)]
+        lib.orc_walk_flight.argtypes = [P(_abi.vmc_scene), P(_abi.vmc_config), u64, u64, C.c_int, vp,
+                                        P(C.c_double)]
         self.lib = lib
 
     def rng_kat(self, seed: int, sid: int, n: int):
@@ -247,6 +249,17 @@ class COracle(_Base):
             out["det"] = det_arr[:min(dcount.value, len(det_arr))]
             out["det_count"] = dcount.value
         return out
+
+
+    def walk_flight(self, scene, config, first, count, threads=1):
+        """K1f's flight decomposition in double precision (traces, dispositions)."""
+        m = Marshalled(scene, config)
+        t_arr = np.zeros(count, dtype=_abi.trace_dtype())
+        disp = (C.c_double * 4)()
+        rc = self.lib.orc_walk_flight(C.byref(m.scene), C.byref(m.config), first, count, threads,
+                                      t_arr.ctypes.data, disp)
+        self._check(rc, self.lib.orc_last_error)
+        return {"traces": t_arr, "disp": list(disp)}
 
 
 _ref_singleton: Optional[RefLib] = None

@@ -426,6 +426,180 @@ static int walk_one(const ctx_t* cx, uint64_t idx, int64_t* cells, vmc_photon_tr
   return 0;
 }
 
+/* The same photon walked in K1f's decomposition (csrc/flight.cuh), in double
+ * precision: one setup per free flight (incremental-DDA face distances tm,
+ * increments td, flight length L = min(remaining_scat / mus, horizon
+ * distance)), faces walked from the flight start (tm += td, the face at s ends
+ * the flight when the neighbour label differs or is exterior), and the
+ * scatter / interface / horizon events of run_photon (transport.cpp:310-358)
+ * between flights. In exact arithmetic this is the reference's walk; the test
+ * (tests/test_oracle_ref.py) checks that in double precision it draws the same
+ * RNG stream per photon as the compiled reference, i.e. that the flight
+ * decomposition changes nothing but rounding. Traces only. */
+static int walk_one_flight(const ctx_t* cx, uint64_t idx, vmc_photon_trace* tr, disp_t* acc) {
+  const vmc_scene* s = cx->s;
+  const vmc_config* c = cx->c;
+  const double h = s->voxel_mm;
+  const double* M = s->media;
+  orc_rng r;
+  orc_rng_seed(&r, c->master_seed, idx);
+  photon_t ph;
+  if (launch(cx, &r, &ph) != 0) return -1;
+  disp_t dp = {0, 0, 0, 0};
+  uint32_t steps = 0, nscat = 0, flags = 0;
+  const double tmax = c->tmax_ns;
+  for (;;) {
+    /* ---- flight setup ---- */
+    const int lab = ph.label;
+    const double mua = M[4 * lab], mus = M[4 * lab + 1], g = M[4 * lab + 2], n = M[4 * lab + 3];
+    const double nspm = n * (1.0 / kC);
+    double tm[3], td[3];
+    int sg[3];
+    for (int k = 0; k < 3; ++k) {
+      const double plane = (ph.v[k] + (ph.d[k] > 0.0 ? 1 : 0)) * h;
+      const double tk = (plane - ph.p[k]) * ph.inv[k];
+      tm[k] = ph.d[k] != 0.0 ? (tk > 0.0 ? tk : 0.0) : INFINITY;
+      td[k] = h * fabs(ph.inv[k]);
+      sg[k] = ph.d[k] > 0.0 ? 1 : -1;
+    }
+    const double ds = mus > 0.0 ? ph.rs / mus : INFINITY;
+    const double left = tmax - ph.t;
+    const int horizon = ds * nspm >= left;
+    const double L = horizon ? fmax(0.0, left / nspm) : ds;
+    double s0 = 0.0;
+    /* ---- walk faces while the next one comes before L ---- */
+    int face = 0, ax = 0;
+    double sf = 0.0;
+    for (;;) {
+      int a = 0;
+      double sm = tm[0];
+      if (tm[1] < sm) {
+        sm = tm[1];
+        a = 1;
+      }
+      if (tm[2] < sm) {
+        sm = tm[2];
+        a = 2;
+      }
+      if (sm >= L) break; /* scatter / horizon win ties (transport.cpp:175, 191) */
+      ++steps;
+      const double w1 = ph.w * exp_neg(mua * (sm - s0));
+      dp.dep += ph.w - w1;
+      ph.w = w1;
+      s0 = sm;
+      ph.v[a] += sg[a];
+      tm[a] += td[a];
+      const int ext = !in_grid(s, ph.v);
+      if (ext || s->labels[lin(s, ph.v)] != lab) {
+        face = 1;
+        ax = a;
+        sf = sm;
+        break;
+      }
+    }
+    if (!face) { /* the flight ends inside the voxel at L */
+      ++steps;
+      const double w1 = ph.w * exp_neg(mua * (L - s0));
+      dp.dep += ph.w - w1;
+      ph.w = w1;
+      for (int k = 0; k < 3; ++k) ph.p[k] += ph.d[k] * L;
+      if (horizon) {
+        ph.t = tmax;
+        dp.trunc += ph.w;
+        flags |= 4u;
+        break;
+      }
+      ph.t += L * nspm;
+      hg_rotate(&ph, g, &r);
+      ph.rs = scat_len(&r);
+      ++nscat;
+      if (ph.w < c->roulette_threshold) {
+        const double before = ph.w;
+        if (orc_rng_unit(&r) < 1.0 / c->roulette_multiplier) {
+          ph.w *= c->roulette_multiplier;
+          dp.kill += before - ph.w;
+        } else {
+          dp.kill += before;
+          flags |= 2u;
+          break;
+        }
+      }
+      continue;
+    }
+    /* ---- interface at the face sf (handle_interface, transport.cpp:227-298) ---- */
+    ph.t += sf * nspm;
+    ph.rs = fmax(0.0, ph.rs - sf * mus);
+    for (int k = 0; k < 3; ++k) ph.p[k] += ph.d[k] * sf;
+    ph.p[ax] = (ph.v[ax] + (sg[ax] > 0 ? 0 : 1)) * h; /* the moved index's near face */
+    const int exterior = !in_grid(s, ph.v);
+    const int nlab = exterior ? 0 : s->labels[lin(s, ph.v)];
+    const double n2 = M[4 * nlab + 3];
+    int exited = 0, back = 0;
+    if (exterior && c->boundary_mode == VMC_BOUNDARY_TERMINATE) {
+      exited = 1;
+    } else if (n == n2) {
+      exited = exterior;
+    } else {
+      const double ci = fabs(ph.d[ax]);
+      const double si2 = fmax(0.0, 1.0 - ci * ci);
+      const double eta = n / n2;
+      const double st2 = eta * eta * si2;
+      if (st2 > 1.0) {
+        back = 1;
+      } else {
+        const double ct = sqrt(1.0 - st2);
+        const double rsp = (n * ci - n2 * ct) / (n * ci + n2 * ct);
+        const double rpp = (n * ct - n2 * ci) / (n * ct + n2 * ci);
+        if (orc_rng_unit(&r) < 0.5 * (rsp * rsp + rpp * rpp)) {
+          back = 1;
+        } else {
+          double nd[3];
+          for (int k = 0; k < 3; ++k) nd[k] = k == ax ? (ph.d[ax] > 0.0 ? ct : -ct) : ph.d[k] * eta;
+          const double kk = 1.0 / sqrt(nd[0] * nd[0] + nd[1] * nd[1] + nd[2] * nd[2]);
+          for (int k = 0; k < 3; ++k) nd[k] *= kk;
+          set_dir(&ph, nd);
+          exited = exterior;
+        }
+      }
+    }
+    if (exited) {
+      dp.esc += ph.w;
+      flags |= 1u;
+      break;
+    }
+    if (back) {
+      double nd[3] = {ph.d[0], ph.d[1], ph.d[2]};
+      nd[ax] = -nd[ax];
+      set_dir(&ph, nd);
+      ph.v[ax] -= sg[ax];
+    } else {
+      ph.label = nlab;
+    }
+  }
+  if (tr) {
+    orc_rng probe;
+    orc_rng_seed(&probe, c->master_seed, idx);
+    uint32_t k = 0;
+    while (!(probe.lo == r.lo && probe.hi == r.hi) && k < (1u << 26)) {
+      orc_rng_next(&probe);
+      ++k;
+    }
+    tr->draws = k;
+    tr->steps = steps;
+    tr->scatters = nscat;
+    tr->flags = flags;
+    tr->deposited = dp.dep;
+    tr->escaped = dp.esc;
+    tr->killed = dp.kill;
+    tr->truncated = dp.trunc;
+  }
+  acc->dep += dp.dep;
+  acc->esc += dp.esc;
+  acc->kill += dp.kill;
+  acc->trunc += dp.trunc;
+  return 0;
+}
+
 typedef struct {
   const ctx_t* cx;
   uint64_t first, lo, hi;
@@ -434,14 +608,17 @@ typedef struct {
   disp_t disp;
   hits_t hits;
   int want_hits;
+  int flight;
   int status;
 } job_t;
 
 static void* run_job(void* arg) {
   job_t* j = (job_t*)arg;
   for (uint64_t k = j->lo; k < j->hi; ++k) {
-    if (walk_one(j->cx, j->first + k, j->cells, j->traces ? j->traces + k : NULL, &j->disp,
-                 j->want_hits ? &j->hits : NULL) != 0) {
+    const int rc = j->flight ? walk_one_flight(j->cx, j->first + k, j->traces ? j->traces + k : NULL, &j->disp)
+                             : walk_one(j->cx, j->first + k, j->cells, j->traces ? j->traces + k : NULL, &j->disp,
+                                        j->want_hits ? &j->hits : NULL);
+    if (rc != 0) {
       j->status = 1;
       return NULL;
     }
@@ -449,9 +626,9 @@ static void* run_job(void* arg) {
   return NULL;
 }
 
-int orc_walk(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count,
-             int threads, int64_t* cells_out, vmc_photon_trace* traces, double* disp4,
-             void* det_out, uint64_t* det_count) {
+static int walk_jobs(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count,
+                     int threads, int64_t* cells_out, vmc_photon_trace* traces, double* disp4,
+                     void* det_out, uint64_t* det_count, int flight) {
   if (s->nx < 1 || s->ny < 1 || s->nz < 1 || !(s->voxel_mm > 0.0) || s->nmedia < 1 ||
       s->nmedia > 256) {
     snprintf(g_err, sizeof g_err, "invalid grid");
@@ -477,6 +654,7 @@ int orc_walk(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t c
     jobs[t].cells = cells_out ? (int64_t*)calloc(ncell, sizeof(int64_t)) : NULL;
     jobs[t].traces = traces;
     jobs[t].want_hits = want_hits;
+    jobs[t].flight = flight;
     pthread_create(&tids[t], NULL, run_job, &jobs[t]);
   }
   int status = 0;
@@ -521,6 +699,17 @@ int orc_walk(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t c
     return 1;
   }
   return 0;
+}
+
+int orc_walk(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count,
+             int threads, int64_t* cells_out, vmc_photon_trace* traces, double* disp4,
+             void* det_out, uint64_t* det_count) {
+  return walk_jobs(s, c, first, count, threads, cells_out, traces, disp4, det_out, det_count, 0);
+}
+
+int orc_walk_flight(const vmc_scene* s, const vmc_config* c, uint64_t first, uint64_t count,
+                    int threads, vmc_photon_trace* traces, double* disp4) {
+  return walk_jobs(s, c, first, count, threads, NULL, traces, disp4, NULL, NULL, 1);
 }
 
 size_t vmc_det_record_bytes(int32_t nmedia) {

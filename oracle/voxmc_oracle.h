@@ -35,6 +35,11 @@ int orc_walk(const vmc_scene* scene, const vmc_config* config, uint64_t first, u
              int threads, int64_t* cells_out, vmc_photon_trace* traces, double* disp4,
              void* det_out, uint64_t* det_count);
 
+/* The same photons walked in the flight kernel's decomposition (K1f,
+ * csrc/flight.cuh) in double precision: per-photon traces and dispositions. */
+int orc_walk_flight(const vmc_scene* scene, const vmc_config* config, uint64_t first, uint64_t count,
+                    int threads, vmc_photon_trace* traces, double* disp4);
+
 const char* orc_last_error(void);
 
 #ifdef __cplusplus
