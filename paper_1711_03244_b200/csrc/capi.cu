@@ -390,6 +390,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   A.rmultf = static_cast<float>(A.rmult);
   A.inv_rmultf = static_cast<float>(A.inv_rmult);
   A.inv_gate_wf = static_cast<float>(A.inv_gate_w);
+  A.gate_wf = static_cast<float>(c->tmax_ns / c->ngates);
   A.qscalef = static_cast<float>(A.qscale);
   A.scatter_pct = env_int("VMC_SCATTER_PCT", 50);
   A.refill_min = env_int("VMC_REFILL_MIN", 1);  // measured: 1 >= 2 > 3 > 4

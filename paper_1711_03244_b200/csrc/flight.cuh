@@ -124,6 +124,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   int sx = 0, sy = 0, sz = 0;  // +-1: direction of travel per axis
   int lab = 0, fax = 0;
   int gate = 0;
+  float gate_end = 0;  // gated launches: the time at which `gate` ends (+inf for the last)
   // this CTA's replica of the fluence map (see KernelArgs::rep_mask); the host
   // keeps rep_mask * rep_stride < 2^31, so the offset is a 32-bit cell index
   const int roff = (static_cast<int>(blockIdx.x) & A.rep_mask) * static_cast<int>(A.rep_stride);
@@ -196,14 +197,23 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
   };
-  auto set_gate = [&](float tt) {
+  // The gate only changes when t passes gate_end, so the common case is one
+  // compare; the gate index itself (gate_of, the semantics) is recomputed only
+  // then. Returns true when the gate changed.
+  auto set_gate = [&](float tt) -> bool {
     if constexpr (kGates) {
-      const int g = gate_of(tt);
-      if (g != gate) {
+      if (tt >= gate_end) {
+        const int g = gate_of(tt);
+        const bool changed = g != gate;
         gate = g;
         gmap = cbase + static_cast<long long>(g) * A.nvox;
+        const float e = static_cast<float>(g + 1) * A.gate_wf;
+        // next boundary; one ulp further if rounding put tt past it in the same gate
+        gate_end = g >= A.ngates - 1 ? Tr::inf() : (e > tt ? e : nextafterf(tt, Tr::inf()));
+        return changed;
       }
     }
+    return false;
   };
   auto add_path = [&](float s) {
     if constexpr (kDet) {
@@ -284,7 +294,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     tf = te;
     rs = 0.0f;
     if constexpr (kGates) {
-      if (gate_of(te) != gate) deposit_run();  // a new gate closes the run
+      if (te >= gate_end && gate_of(te) != gate) deposit_run();  // a new gate closes the run
       set_gate(te);
     }
     phase = SCAT;
@@ -585,6 +595,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if constexpr (kGates) {
       gate = 0;
       gmap = cbase;
+      gate_end = A.ngates > 1 ? A.gate_wf : Tr::inf();
     }
     if constexpr (kTrace) {
       steps = nscat = 0;

@@ -101,7 +101,7 @@ struct KernelArgs {
   // K1f (flight.cuh): the event-phase trigger (percent of live lanes that
   // must have finished their flight before the warp runs the event phase)
   int stash_off;  // K1f: byte offset of the per-warp seed stashes (kBlock / 32 x 656 B)
-  int pad9;
+  float gate_wf;  // K1f: gate width tmax / ngates (FP32)
   int event_pct;
   int absorb_mode;  // K1f absorb(): max mua*h*sqrt(3) < 0.012 -> 0, < 0.15 -> 1, else 2
   // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
