@@ -699,6 +699,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if (phase == ENDF) end_flight();
     if (phase == SCAT || phase == RETRY) scatter();
     if (phase == FACE) face();
+    __syncwarp();  // reconverge before the shared flight setup (face() has warp-level votes)
     if (phase == SETUP) setup();
     // ================= walk phase =================
     // every lane in flight crosses faces until at most (100 - event_pct) % of
