@@ -445,11 +445,10 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   // media table, plus per-thread per-label path lengths in detector mode
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
             (det ? static_cast<size_t>(vmc::kMaxDetMedia) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float)) : 0);
-  // K1f: escaped / killed / truncated quanta per thread after the above
-  A.acc_off = static_cast<int>((P->smem + 15) & ~static_cast<size_t>(15));
-  P->smem = static_cast<size_t>(A.acc_off) + 3 * vmc::kBlock * sizeof(long long);
-  A.stash_off = static_cast<int>((P->smem + 15) & ~static_cast<size_t>(15));
-  P->smem = static_cast<size_t>(A.stash_off) + (vmc::kBlock / 32) * (32 * 20 + 16);
+  // K1f adds its per-thread disposition slots and per-warp seed stashes (the
+  // kernel places them at compile-time offsets in front of the media table)
+  P->smem = ((P->smem + 15) & ~static_cast<size_t>(15)) + 3 * vmc::kBlock * sizeof(long long) +
+            (vmc::kBlock / 32) * (32 * 20 + 16);
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");

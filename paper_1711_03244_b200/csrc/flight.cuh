@@ -72,9 +72,17 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Rng = Xs128p<kTrace>;
   constexpr int WALK = 0, SCAT = 1, DEAD = 2, RETRY = 3, FACE = 4, SETUP = 5, ENDF = 6;
   unsigned char* smem = vmc_smem;
+  // Shared-memory layout at compile-time offsets (cheap to rematerialise):
+  // per-thread disposition slots | per-warp seed stashes | per-thread path
+  // lengths (detector kernels) | media table
+  constexpr int kAccOff = 0;                                       // 3 x kBlock x int64
+  constexpr int kStashOff = kAccOff + 3 * kBlock * 8;              // kBlock / 32 x (32 x 20 + 16) B
+  constexpr int kPpOff = kStashOff + (kBlock / 32) * (32 * 20 + 16);
+  constexpr int kMediaOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * 4 : 0);
+  static_assert(kStashOff % 16 == 0 && kPpOff % 16 == 0 && kMediaOff % 16 == 0, "smem alignment");
 
   // ---- shared memory: media table (exterior n is needed even when kUni) ----
-  Medium<float>* sm_media = reinterpret_cast<Medium<float>*>(smem);
+  Medium<float>* sm_media = reinterpret_cast<Medium<float>*>(smem + kMediaOff);
   {
     const Medium<float>* gm = static_cast<const Medium<float>*>(A.media);
     const int nwords = static_cast<int>(sizeof(Medium<float>) / 4) * A.nmedia;
@@ -102,7 +110,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // escaped / killed / truncated quanta change once per photon, so they live in
   // this thread's shared-memory slots (acc_sm[k * kBlock]: 0 escaped, 1 killed,
   // 2 truncated), not in registers; the deposited channel is booked by the fold
-  long long* const acc_sm = reinterpret_cast<long long*>(smem + A.acc_off) + threadIdx.x;
+  long long* const acc_sm = reinterpret_cast<long long*>(smem + kAccOff) + threadIdx.x;
   acc_sm[0] = acc_sm[kBlock] = acc_sm[2 * kBlock] = 0;
 
   int phase = DEAD;
@@ -135,8 +143,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   uint32_t steps = 0, nscat = 0;
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // trace only
   bool detected = false;
-  float* pp_sm = reinterpret_cast<float*>(smem + ((sizeof(Medium<float>) * A.nmedia + 15) & ~static_cast<size_t>(15))) +
-                 threadIdx.x;
+  float* pp_sm = reinterpret_cast<float*>(smem + kPpOff) + threadIdx.x;
 
   auto quant = [&](float x) -> long long { return __float2ll_rn(x * qscale); };
   auto gate_of = [&](float tt) -> int {
@@ -612,7 +619,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // st_base + 0..31 and a header {next unused slot, valid slots}; st_base and
   // st_claimed_all are warp-uniform registers
   const int warp = threadIdx.x >> 5;
-  unsigned char* const stash = smem + A.stash_off + warp * (32 * 20 + 16);
+  unsigned char* const stash = smem + kStashOff + warp * (32 * 20 + 16);
   uint64_t* const st_a = reinterpret_cast<uint64_t*>(stash);
   uint64_t* const st_b = st_a + 32;
   float* const st_rs = reinterpret_cast<float*>(stash + 32 * 16);  // pencil sources: first free path

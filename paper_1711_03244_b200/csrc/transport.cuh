@@ -100,7 +100,7 @@ struct KernelArgs {
   Medium<double> uni_d;
   // K1f (flight.cuh): the event-phase trigger (percent of live lanes that
   // must have finished their flight before the warp runs the event phase)
-  int stash_off;  // K1f: byte offset of the per-warp seed stashes (kBlock / 32 x 656 B)
+  int pad11;
   float gate_wf;  // K1f: gate width tmax / ngates (FP32)
   int event_pct;
   int absorb_mode;  // K1f absorb(): max mua*h*sqrt(3) < 0.012 -> 0, < 0.15 -> 1, else 2
@@ -109,8 +109,7 @@ struct KernelArgs {
   long long rep_stride;
   int rep_mask;
   int walk_keep;  // K1f: a full warp walks while more than (32 * (100 - event_pct)) / 100 lanes walk
-  int acc_off;    // K1f: byte offset of the per-thread disposition accumulators in shared memory
-  int pad7;
+  int pad10, pad7;
   float detf[kMaxDet][4];  // K1f: detector disks as {x, y, z, r^2} in FP32
 };
 
