@@ -703,6 +703,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         }
       }
     }
+    // multi-label kernels: reconverge after the refill (+3 % B3, +1.5 % head;
+    // the single-label kernel is ~0.4 % faster without)
+    if constexpr (!kUni) __syncwarp();
     if (phase == ENDF) end_flight();
     if (phase == SCAT || phase == RETRY) scatter();
     if (phase == FACE) face();
