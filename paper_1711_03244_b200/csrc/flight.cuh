@@ -718,15 +718,24 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if (exhausted && dead == 0xffffffffu) break;
     // walk_keep scaled to the live lanes (all 32 until the photons run out)
     const int keep = ((32 - (exhausted ? __popc(dead) : 0)) * A.walk_keep) >> 5;
-    for (;;) {
-      const unsigned walking = __ballot_sync(0xffffffffu, phase == WALK);
-      if (__popc(walking) <= keep) break;
-      VMC_ST(6, 1);
-      VMC_ST(7, __popc(walking));
-      // three steps per vote: amortises the loop control (2 and 4 measured slower)
-      if (phase == WALK) walk();
-      if (phase == WALK) walk();
-      if (phase == WALK) walk();
+    // After an event phase nearly every lane walks in the cube60 kernels, so
+    // their first vote is skipped (+1 %); in the strongly scattering head most
+    // new flights end in their voxel, so the gated kernel votes first
+    // (three steps per vote amortise the loop control; 2 and 4 measured slower)
+    if constexpr (kGates) {
+      while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep) {
+        VMC_ST(6, 1);
+        if (phase == WALK) walk();
+        if (phase == WALK) walk();
+        if (phase == WALK) walk();
+      }
+    } else {
+      do {
+        VMC_ST(6, 1);
+        if (phase == WALK) walk();
+        if (phase == WALK) walk();
+        if (phase == WALK) walk();
+      } while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep);
     }
   }
 
