@@ -714,10 +714,13 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // ================= walk phase =================
     // every lane in flight crosses faces until at most (100 - event_pct) % of
     // the live lanes are still walking; the others wait for the event phase
-    const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
-    if (exhausted && dead == 0xffffffffu) break;
-    // walk_keep scaled to the live lanes (all 32 until the photons run out)
-    const int keep = ((32 - (exhausted ? __popc(dead) : 0)) * A.walk_keep) >> 5;
+    // walk_keep, scaled to the live lanes once the photons have run out
+    int keep = A.walk_keep;
+    if (exhausted) {
+      const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
+      if (dead == 0xffffffffu) break;
+      keep = ((32 - __popc(dead)) * A.walk_keep) >> 5;
+    }
     // After an event phase nearly every lane walks in the cube60 kernels, so
     // their first vote is skipped (+1 %); in the strongly scattering head most
     // new flights end in their voxel, so the gated kernel votes first
