@@ -144,6 +144,27 @@ def test_determinism_and_range_split(gpu):
     assert tuple(int(x) for x in q) == a.totals_q
 
 
+@pytest.mark.parametrize("name", ["b2", "b3"])
+def test_tiny_and_ragged_ranges(gpu, name):
+    """Claims go 32 photons at a time through the per-warp seed stash: ranges of
+    1, 31, 32, 33 ... photons at odd offsets must still give, summed, the map of
+    one launch over the union, bit for bit."""
+    st = setup(name, n=1_000)
+    whole = gpu.run_group_dynamic(0, 1_000, 1, st.scene, st.config)
+    acc = np.zeros_like(whole.map.cells)
+    q = np.zeros(4, dtype=np.int64)
+    first = 0
+    for cnt in (1, 31, 32, 33, 1, 64, 65, 2, 771):
+        r = gpu.run_group_dynamic(first, cnt, 1, st.scene, st.config)
+        acc += r.map.cells
+        q += np.array(r.totals_q)
+        first += cnt
+    assert first == 1_000
+    assert np.array_equal(acc, whole.map.cells)
+    assert tuple(int(x) for x in q) == whole.totals_q
+    assert gpu.run_group_dynamic(5, 0, 1, st.scene, st.config).totals_q == (0, 0, 0, 0)
+
+
 @pytest.mark.parametrize("name", ["b1", "b3"])
 def test_map_replicas_bit_identical(gpu, monkeypatch, name):
     """Fluence-map replicas (CTA b adds into copy b mod R, one fold kernel sums
