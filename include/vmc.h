@@ -226,6 +226,11 @@ VMC_API int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t 
 /* FNV-1a 64 of a byte buffer (the reference's volume checksum, volume_io.cpp:13-20). Host only. */
 VMC_API uint64_t vmc_fnv1a64(const void* data, size_t bytes);
 
+/* Mangled device symbol of the transport kernel variant this plan launches
+ * (e.g. _ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi1EEEvNS_10KernelArgsE = the FP32
+ * gated multi-label Taylor-5 K1f); "" when unavailable. Valid while the plan lives. */
+VMC_API const char* vmc_plan_kernel_name(const vmc_plan* plan);
+
 /* Number of kernels vmc_plan_run enqueues per call (for launch accounting). */
 VMC_API int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags);
 

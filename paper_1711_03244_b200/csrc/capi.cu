@@ -34,6 +34,7 @@ namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
 const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode);
+const void* flight_kernel_double(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
 namespace {
@@ -289,6 +290,7 @@ struct vmc_plan {
   int grid = 0, grid_trace = 0;
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
+  std::string kern_name;  // mangled device symbol of `kern` (cudaFuncGetName)
   // fluence-map scratch: nrep replicas (nrep > 1 for small maps) the transport
   // kernel deposits into, folded into the caller's map after each launch. K1f
   // always deposits into the scratch: the fold also books the deposited channel
@@ -428,19 +430,30 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     const double xmax = mx * s->voxel_mm * std::sqrt(3.0);
     A.absorb_mode = xmax < 0.012 ? 0 : (xmax < 0.15 ? 1 : 2);
   }
-  // FP32: K1f (flight.cuh) unless VMC_KERNEL=step selects the per-step K1
-  // (transport.cuh) for A/B runs; FP64 parity mode always runs K1.
+  // K1f (flight.cuh) in the launch's precision unless VMC_KERNEL=step selects
+  // the per-step K1 (transport.cuh) for A/B runs. FP64 K1f is the
+  // exact-arithmetic pin of the product kernel's structure.
   const char* kk = std::getenv("VMC_KERNEL");
   const bool step_kernel = kk && std::strcmp(kk, "step") == 0;
-  if (f64) {
-    P->kern = vmc::transport_kernel_double(gates, det, false, uniform);
-    P->kern_trace = vmc::transport_kernel_double(gates, det, true, uniform);
-  } else if (step_kernel) {
-    P->kern = vmc::transport_kernel_float(gates, det, false, uniform);
-    P->kern_trace = vmc::transport_kernel_float(gates, det, true, uniform);
+  if (step_kernel) {
+    P->kern = f64 ? vmc::transport_kernel_double(gates, det, false, uniform)
+                  : vmc::transport_kernel_float(gates, det, false, uniform);
+    P->kern_trace = f64 ? vmc::transport_kernel_double(gates, det, true, uniform)
+                        : vmc::transport_kernel_float(gates, det, true, uniform);
+  } else if (f64) {
+    P->kern = vmc::flight_kernel_double(gates, det, false, uniform);
+    P->kern_trace = vmc::flight_kernel_double(gates, det, true, uniform);
   } else {
-    P->kern = vmc::flight_kernel_float(gates, det, false, uniform, A.absorb_mode);
-    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, A.absorb_mode);
+    // VMC_GENERIC_ABSORB=1 (test hook): the generic variant that picks its
+    // absorb series at run time instead of the compiled-in production one
+    const int abs_sel = env_int("VMC_GENERIC_ABSORB", 0) ? -1 : A.absorb_mode;
+    P->kern = vmc::flight_kernel_float(gates, det, false, uniform, abs_sel);
+    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, abs_sel);
+  }
+  {
+    const char* nm = nullptr;
+    if (cudaFuncGetName(&nm, P->kern) == cudaSuccess && nm) P->kern_name = nm;
+    else cudaGetLastError();
   }
   // media table, plus per-thread per-label path lengths in detector mode
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
@@ -448,7 +461,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   // K1f adds its per-thread disposition slots and per-warp seed stashes (the
   // kernel places them at compile-time offsets in front of the media table)
   P->smem = ((P->smem + 15) & ~static_cast<size_t>(15)) + 3 * vmc::kBlock * sizeof(long long) +
-            (vmc::kBlock / 32) * (32 * 20 + 16);
+            (vmc::kBlock / 32) * vmc::flight_stash_bytes(f64 ? sizeof(double) : sizeof(float));
   P->smem_trace = P->smem;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
@@ -477,7 +490,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     int p2 = 1;
     while (p2 * 2 <= std::max(1, r)) p2 *= 2;
     P->nrep = p2;
-    P->fold_books_deposited = !f64 && !step_kernel;  // K1f keeps no deposited accumulator
+    P->fold_books_deposited = !step_kernel;  // K1f keeps no deposited accumulator
     P->scratch = P->nrep > 1 || P->fold_books_deposited;
     if (P->scratch) get(P->rep, cache ? &cache->rep : nullptr, static_cast<size_t>(P->nrep) * map_bytes);
     A.rep_mask = P->nrep - 1;
@@ -1211,6 +1224,8 @@ uint64_t vmc_fnv1a64(const void* data, size_t bytes) {
   }
   return h;
 }
+
+const char* vmc_plan_kernel_name(const vmc_plan* plan) { return plan ? plan->kern_name.c_str() : ""; }
 
 int vmc_plan_launches_per_run(const vmc_plan* plan, uint32_t flags) {
   (void)flags;

@@ -1,4 +1,4 @@
-// flight.cuh — K1f, the FP32 photon-transport kernel organised by free flight (sm_100a).
+// flight.cuh — K1f, the photon-transport kernel organised by free flight (sm_100a).
 //
 // Same photons, same RNG draws in the same order, same discrete decisions as
 // run_photon (proj/core/src/transport.cpp:310-358); what changes is how a warp
@@ -38,6 +38,16 @@
 // accumulated from the flight start instead of recomputed per face), which moves no
 // discrete decision beyond the per-photon draw-count gates of the parity tests.
 //
+// Two arithmetic instantiations of the same body:
+//   float  — the product path (MUFU transcendentals, FP32 Taylor absorb,
+//            deposits coalesced per (voxel, gate) run, u = top 24 bits);
+//   double — the exact-arithmetic pin of the product kernel's structure
+//            (compiled with --fmad=false): the reference's own formulas op for
+//            op (exp_neg, hg_cos_theta, the azimuth rejection, Fresnel, Snell,
+//            u = top 53 bits, libm-style log/exp/sqrt) and one llround deposit
+//            per step like FluenceMap::deposit, so each photon's dispositions
+//            match the reference to ~1e-12 whenever its discrete path does.
+//
 // Deposits go into one of KernelArgs::rep_mask + 1 replicas of the map (CTA
 // index mod replicas): the voxels next to the source take every photon's
 // first deposits, and spreading them over replicas keeps the same-address
@@ -62,37 +72,95 @@ __device__ unsigned long long vmc_flight_stats[12];
 __device__ unsigned int vmc_flight_done;
 #endif
 
+// The arithmetic that differs between the FP32 product path and the FP64 pin.
+template <typename Real>
+struct FlightOps;
+
+template <>
+struct FlightOps<float> {
+  static constexpr bool kF32 = true;
+  using Tr = RealTraits<float>;
+  static __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+  static __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+  static __device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+  static __device__ __forceinline__ bool neg(float a) { return __float_as_int(a) < 0; }
+  static __device__ __forceinline__ float up(float a) { return nextafterf(a, Tr::inf()); }
+  static __device__ __forceinline__ float pick(float f, double) { return f; }
+  static __device__ __forceinline__ long long quant(float x, float qscale) { return __float2ll_rn(x * qscale); }
+  // 2u - 1 for the rejection azimuth, exact from the top 24 bits
+  template <class Rng>
+  static __device__ __forceinline__ float two_u_m1(Rng& r) {
+    return fmaf(r.u24(), 0x1p-23f, -1.0f);
+  }
+  // -log(u) (transport.cpp:14-17); u = 0 (p = 2^-24) stands for [0, 2^-24): 2^-25
+  template <class Rng>
+  static __device__ __forceinline__ float scat_len(Rng& r) {
+    const float u = r.template unit<float>();
+    return -Tr::ln(u > 0.0f ? u : 0x1p-25f);
+  }
+};
+
+template <>
+struct FlightOps<double> {
+  static constexpr bool kF32 = false;
+  using Tr = RealTraits<double>;
+  static __device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+  static __device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+  static __device__ __forceinline__ double vabs(double a) { return fabs(a); }
+  static __device__ __forceinline__ bool neg(double a) { return __double_as_longlong(a) < 0; }
+  static __device__ __forceinline__ double up(double a) { return nextafter(a, Tr::inf()); }
+  static __device__ __forceinline__ double pick(float, double d) { return d; }
+  static __device__ __forceinline__ long long quant(double x, double qscale) { return llround(x * qscale); }
+  template <class Rng>
+  static __device__ __forceinline__ double two_u_m1(Rng& r) {
+    return 2.0 * r.template unit<double>() - 1.0;
+  }
+  template <class Rng>
+  static __device__ __forceinline__ double scat_len(Rng& r) {
+    const double u = r.template unit<double>();
+    return -log(u > 0.0 ? u : 4.9406564584124654e-324);
+  }
+};
+
 // kAbs: -1 = absorb() picks its series per launch (KernelArgs::absorb_mode);
 // 0 / 1 = compiled for absorb_mode 0 (every mua * h * sqrt(3) < 0.012, the
 // cube60 phantoms) / 1 (< 0.15, the head phantom), which drops the warp-uniform
-// mode tests from every absorb()
-template <bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1>
+// mode tests from every absorb(). The double instantiation always uses the
+// reference's exp_neg.
+template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
-  using Tr = RealTraits<float>;
+  using Tr = RealTraits<Real>;
+  using F = FlightOps<Real>;
+  constexpr bool kF32 = F::kF32;
   using Rng = Xs128p<kTrace>;
   constexpr int WALK = 0, SCAT = 1, DEAD = 2, RETRY = 3, FACE = 4, SETUP = 5, ENDF = 6;
   unsigned char* smem = vmc_smem;
   // Shared-memory layout at compile-time offsets (cheap to rematerialise):
   // per-thread disposition slots | per-warp seed stashes | per-thread path
   // lengths (detector kernels) | media table
+  constexpr int kStashBytes = flight_stash_bytes(sizeof(Real));
   constexpr int kAccOff = 0;                                       // 3 x kBlock x int64
-  constexpr int kStashOff = kAccOff + 3 * kBlock * 8;              // kBlock / 32 x (32 x 20 + 16) B
-  constexpr int kPpOff = kStashOff + (kBlock / 32) * (32 * 20 + 16);
-  constexpr int kMediaOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * 4 : 0);
+  constexpr int kStashOff = kAccOff + 3 * kBlock * 8;              // kBlock / 32 x kStashBytes
+  constexpr int kPpOff = kStashOff + (kBlock / 32) * kStashBytes;
+  constexpr int kMediaOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * static_cast<int>(sizeof(Real)) : 0);
   static_assert(kStashOff % 16 == 0 && kPpOff % 16 == 0 && kMediaOff % 16 == 0, "smem alignment");
 
   // ---- shared memory: media table (exterior n is needed even when kUni) ----
-  Medium<float>* sm_media = reinterpret_cast<Medium<float>*>(smem + kMediaOff);
+  Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem + kMediaOff);
   {
-    const Medium<float>* gm = static_cast<const Medium<float>*>(A.media);
-    const int nwords = static_cast<int>(sizeof(Medium<float>) / 4) * A.nmedia;
+    const Medium<Real>* gm = static_cast<const Medium<Real>*>(A.media);
+    const int nwords = static_cast<int>(sizeof(Medium<Real>) / 4) * A.nmedia;
     for (int i = threadIdx.x; i < nwords; i += blockDim.x)
       reinterpret_cast<int*>(sm_media)[i] = reinterpret_cast<const int*>(gm)[i];
   }
   __syncthreads();
-  auto medium = [&](int l) -> const Medium<float>& {
+  auto medium = [&](int l) -> const Medium<Real>& {
     if constexpr (kUni) {
-      return A.uni_f;
+      if constexpr (kF32) {
+        return A.uni_f;
+      } else {
+        return A.uni_d;
+      }
     } else {
       return sm_media[l];
     }
@@ -101,9 +169,9 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   const int nx = A.nx;
   const int ny = A.ny, nz = A.nz;
   const int nxy = static_cast<int>(A.nxy);
-  const float h = A.hf;
-  const float tmax = A.tmaxf;
-  const float qscale = A.qscalef;
+  const Real h = F::pick(A.hf, A.h);
+  const Real tmax = F::pick(A.tmaxf, A.tmax);
+  const Real qscale = F::pick(A.qscalef, A.qscale);
   const int lane = threadIdx.x & 31;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -119,87 +187,97 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   Rng rng;
   rng.a = rng.b = 0;
   // photon state at the start of the current flight
-  float px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 1;
-  float w = 0, tf = 0, rs = 0;  // weight at distance s0 along the flight; time and
-                                // remaining scattering length at the flight start
-  float s0 = 0;      // distance along the flight of the last face (or the flight start)
-  float run_w0 = 0;  // weight at the start of the open deposit run (one voxel, one gate)
-  float L = 0;       // flight length; sign bit set = the flight ends at the horizon.
-                     // FACE: distance of the face event
+  Real px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 1;
+  Real w = 0, tf = 0, rs = 0;  // weight at distance s0 along the flight; time and
+                               // remaining scattering length at the flight start
+  Real s0 = 0;      // distance along the flight of the last face (or the flight start)
+  Real run_w0 = 0;  // weight at the start of the open deposit run (one voxel, one gate)
+  Real L = 0;       // flight length; sign bit set = the flight ends at the horizon.
+                    // FACE: distance of the face event
   // incremental DDA
-  float tmx = 0, tmy = 0, tmz = 0, tdx = 0, tdy = 0, tdz = 0;
+  Real tmx = 0, tmy = 0, tmz = 0, tdx = 0, tdy = 0, tdz = 0;
   int vx = 0, vy = 0, vz = 0;  // voxel coordinates
   int sx = 0, sy = 0, sz = 0;  // +-1: direction of travel per axis
   int lab = 0, fax = 0;
   int gate = 0;
-  float gate_end = 0;  // gated launches: the time at which `gate` ends (+inf for the last)
+  Real gate_end = 0;  // gated launches: the time at which `gate` ends (+inf for the last)
   // this CTA's replica of the fluence map (see KernelArgs::rep_mask); the host
   // keeps rep_mask * rep_stride < 2^31, so the offset is a 32-bit cell index
   const int roff = (static_cast<int>(blockIdx.x) & A.rep_mask) * static_cast<int>(A.rep_stride);
   unsigned long long* const cbase = reinterpret_cast<unsigned long long*>(A.cells) + roff;
   unsigned long long* gmap = cbase;  // cells of `gate` (gated launches)
-  float fmua = 0, fns = 0;  // current medium (multi-label volumes): mua, n / c
-  float sct = 0, sst = 0;  // scatter: cos/sin theta kept across azimuth retries
+  Real fmua = 0, fns = 0;  // current medium (multi-label volumes): mua, n / c
+  Real sct = 0, sst = 0;  // scatter: cos/sin theta kept across azimuth retries
   uint32_t steps = 0, nscat = 0;
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // trace only
   bool detected = false;
-  float* pp_sm = reinterpret_cast<float*>(smem + kPpOff) + threadIdx.x;
+  Real* pp_sm = reinterpret_cast<Real*>(smem + kPpOff) + threadIdx.x;
 
-  auto quant = [&](float x) -> long long { return __float2ll_rn(x * qscale); };
-  auto gate_of = [&](float tt) -> int {
-    const int g = static_cast<int>(tt * A.inv_gate_wf);  // tt >= 0: truncation == floor
+  auto quant = [&](Real x) -> long long { return F::quant(x, qscale); };
+  auto gate_of = [&](Real tt) -> int {
+    const int g = static_cast<int>(tt * F::pick(A.inv_gate_wf, A.inv_gate_w));  // tt >= 0: truncation == floor
     return g < A.ngates - 1 ? g : A.ngates - 1;
   };
-  auto mua_ = [&]() -> float {
+  auto mua_ = [&]() -> Real {
     if constexpr (kUni) {
-      return A.uni_f.mua;
+      return medium(0).mua;
     } else {
       return fmua;
     }
   };
-  auto nsmm_ = [&]() -> float {
+  auto nsmm_ = [&]() -> Real {
     if constexpr (kUni) {
-      return A.uni_f.ns_per_mm;
+      return medium(0).ns_per_mm;
     } else {
       return fns;
     }
   };
   // Beer-Lambert over the segment [s0, s] of the flight (exp_neg,
-  // transport.cpp:22-27): w -= w (1 - exp(-x)) in one rounding, with
-  // 1 - exp(-x) from its Taylor series, so a run's deposit run_w0 - w (exact
-  // by Sterbenz) keeps the step kernel's precision and the weights telescope
-  // exactly. The series order is chosen per launch (warp-uniform branch) from
-  // the largest mua * h * sqrt(3) of the volume: x^3 below 0.012, x^5 below
-  // 0.15 (truncation < 1e-7 relative), else x^5 with a MUFU.EX2 fallback
-  auto absorb = [&](float s) {
-    const float x = mua_() * (s - s0);
-    float f;
-    if (kAbs == 0 || (kAbs < 0 && A.absorb_mode == 0)) {
-      f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f)));
-    } else {
-      f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f - x * (1.0f / 120.0f)))));
-      if (kAbs < 0 && A.absorb_mode == 2 && x >= 0.15f) {
-        float e;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
-        f = 1.0f - e;
+  // transport.cpp:22-27).
+  // FP32: w -= w (1 - exp(-x)) in one rounding, with 1 - exp(-x) from its
+  // Taylor series, so a run's deposit run_w0 - w (exact by Sterbenz) keeps the
+  // step kernel's precision and the weights telescope exactly. The series
+  // order is chosen per launch (warp-uniform branch) from the largest
+  // mua * h * sqrt(3) of the volume: x^3 below 0.012, x^5 below 0.15
+  // (truncation < 1e-7 relative), else x^5 with a MUFU.EX2 fallback.
+  // FP64: w *= exp_neg(x), the reference's degree-4 series below 0.01, else exp.
+  auto absorb = [&](Real s) {
+    const Real x = mua_() * (s - s0);
+    if constexpr (kF32) {
+      float f;
+      if (kAbs == 0 || (kAbs < 0 && A.absorb_mode == 0)) {
+        f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f)));
+      } else {
+        f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f - x * (1.0f / 120.0f)))));
+        if (kAbs < 0 && A.absorb_mode == 2 && x >= 0.15f) {
+          float e;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+          f = 1.0f - e;
+        }
       }
+      w = fmaf(-w, f, w);
+    } else {
+      const double e = x < 0.01 ? 1.0 - x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0)))) : exp(-x);
+      w = w * e;
     }
-    w = fmaf(-w, f, w);
     s0 = s;
   };
   auto cell = [&]() -> int { return vx + nx * vy + nxy * vz; };  // x-fastest linear index (two IMAD)
   // close the open deposit run at weight w_new: one fixed-point add into the
   // voxel the run belongs to (the map is L2-resident for cube60)
   auto deposit_run = [&]() {
-    const float dw = run_w0 - w;
+    const Real dw = run_w0 - w;
     const long long q = quant(dw);
-    // q == 0 only if mua == 0; ungated launches index from the parameter-bank
-    // base (one IMAD.WIDE), gated ones from the gate's pointer
-    if constexpr (kGates) {
-      atomicAdd(gmap + cell(), static_cast<unsigned long long>(q));
-    } else {
-      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + cell()),
-                static_cast<unsigned long long>(q));
+    // FP32: q == 0 only if mua == 0; ungated launches index from the
+    // parameter-bank base (one IMAD.WIDE), gated ones from the gate's pointer.
+    // FP64: one run per step; empty steps add nothing (run_photon :325-328)
+    if (kF32 || q != 0) {
+      if constexpr (kGates) {
+        atomicAdd(gmap + cell(), static_cast<unsigned long long>(q));
+      } else {
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + cell()),
+                  static_cast<unsigned long long>(q));
+      }
     }
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
@@ -207,31 +285,27 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // The gate only changes when t passes gate_end, so the common case is one
   // compare; the gate index itself (gate_of, the semantics) is recomputed only
   // then. Returns true when the gate changed.
-  auto set_gate = [&](float tt) -> bool {
+  auto set_gate = [&](Real tt) -> bool {
     if constexpr (kGates) {
       if (tt >= gate_end) {
         const int g = gate_of(tt);
         const bool changed = g != gate;
         gate = g;
         gmap = cbase + static_cast<long long>(g) * A.nvox;
-        const float e = static_cast<float>(g + 1) * A.gate_wf;
+        const Real e = static_cast<Real>(g + 1) * F::pick(A.gate_wf, A.tmax / A.ngates);
         // next boundary; one ulp further if rounding put tt past it in the same gate
-        gate_end = g >= A.ngates - 1 ? Tr::inf() : (e > tt ? e : nextafterf(tt, Tr::inf()));
+        gate_end = g >= A.ngates - 1 ? Tr::inf() : (e > tt ? e : F::up(tt));
         return changed;
       }
     }
     return false;
   };
-  auto add_path = [&](float s) {
+  auto add_path = [&](Real s) {
     if constexpr (kDet) {
       if (lab >= 1) pp_sm[(lab - 1) * kBlock] += s;
     }
   };
-  auto scat_len_of = [&](Rng& r) -> float {  // transport.cpp:14-17
-    const float u = r.template unit<float>();
-    return -Tr::ln(u > 0.0f ? u : 0x1p-25f);
-  };
-  auto scat_len = [&]() -> float { return scat_len_of(rng); };
+  auto scat_len = [&]() -> Real { return F::scat_len(rng); };
   auto finish = [&](int kind) {  // 0 escaped 1 killed 2 truncated
     if constexpr (kTrace) {
       vmc_photon_trace tr;
@@ -251,55 +325,62 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 
   // ---- flight setup: DDA state and flight length from the current state ----
   auto setup = [&]() {
-    const Medium<float>& M = medium(lab);
+    const Medium<Real>& M = medium(lab);
     if constexpr (!kUni) {
       fmua = M.mua;
       fns = M.ns_per_mm;
     }
-    s0 = 0.0f;
-    const float ix = Tr::rcp(dx), iy = Tr::rcp(dy), iz = Tr::rcp(dz);  // +-inf for 0
+    s0 = Real(0);
+    const Real ix = Tr::rcp(dx), iy = Tr::rcp(dy), iz = Tr::rcp(dz);  // +-inf for 0
     const int ux = vx, uy = vy, uz = vz;
-    const float t0 = (static_cast<float>(ux + (dx > 0.0f ? 1 : 0)) * h - px) * ix;
-    const float t1 = (static_cast<float>(uy + (dy > 0.0f ? 1 : 0)) * h - py) * iy;
-    const float t2 = (static_cast<float>(uz + (dz > 0.0f ? 1 : 0)) * h - pz) * iz;
-    tmx = dx != 0.0f ? fmaxf(t0, 0.0f) : Tr::inf();
-    tmy = dy != 0.0f ? fmaxf(t1, 0.0f) : Tr::inf();
-    tmz = dz != 0.0f ? fmaxf(t2, 0.0f) : Tr::inf();
-    tdx = h * fabsf(ix);
-    tdy = h * fabsf(iy);
-    tdz = h * fabsf(iz);
-    sx = dx > 0.0f ? 1 : -1;
-    sy = dy > 0.0f ? 1 : -1;
-    sz = dz > 0.0f ? 1 : -1;
-    const float ds = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
-    const float rem = tmax - tf;
-    const float dh = fmaxf(0.0f, rem * M.mm_per_ns);
+    const Real t0 = (static_cast<Real>(ux + (dx > Real(0) ? 1 : 0)) * h - px) * ix;
+    const Real t1 = (static_cast<Real>(uy + (dy > Real(0) ? 1 : 0)) * h - py) * iy;
+    const Real t2 = (static_cast<Real>(uz + (dz > Real(0) ? 1 : 0)) * h - pz) * iz;
+    tmx = dx != Real(0) ? F::vmax(t0, Real(0)) : Tr::inf();
+    tmy = dy != Real(0) ? F::vmax(t1, Real(0)) : Tr::inf();
+    tmz = dz != Real(0) ? F::vmax(t2, Real(0)) : Tr::inf();
+    tdx = h * F::vabs(ix);
+    tdy = h * F::vabs(iy);
+    tdz = h * F::vabs(iz);
+    sx = dx > Real(0) ? 1 : -1;
+    sy = dy > Real(0) ? 1 : -1;
+    sz = dz > Real(0) ? 1 : -1;
+    Real ds, dh;
+    const Real rem = tmax - tf;
+    if constexpr (kF32) {
+      ds = M.mus > 0.0f ? rs * M.inv_mus : Tr::inf();  // rs may be 0 after a clamp
+      dh = fmaxf(0.0f, rem * M.mm_per_ns);
+    } else {
+      ds = M.mus > 0.0 ? rs / M.mus : Tr::inf();  // transport.cpp:166, 172
+      dh = fmax(0.0, rem / M.ns_per_mm);
+    }
     L = ds * M.ns_per_mm >= rem ? -dh : ds;  // horizon (transport.cpp:173-175) marked by the sign
     // a flight that ends before the first face skips the walk (short flights:
     // most of them in the head phantom's white matter)
-    phase = fminf(tmx, fminf(tmy, tmz)) >= fabsf(L) ? ENDF : WALK;
+    phase = F::vmin(tmx, F::vmin(tmy, tmz)) >= F::vabs(L) ? ENDF : WALK;
   };
 
   // ---- the flight ended inside the current voxel (ENDF, event phase):
   // scattering point or horizon ----
   auto end_flight = [&]() {
     if constexpr (kTrace) ++steps;
-    const float Ls = fabsf(L);
+    const Real Ls = F::vabs(L);
     absorb(Ls);
     px += dx * Ls;
     py += dy * Ls;
     pz += dz * Ls;
-    const float te = tf + Ls * nsmm_();
+    const Real te = tf + Ls * nsmm_();
     add_path(Ls);
-    if (__float_as_int(L) < 0) {  // StepKind::Terminated (transport.cpp:181-187, 330-332)
+    if (F::neg(L)) {  // StepKind::Terminated (transport.cpp:181-187, 330-332)
       deposit_run();
       acc_sm[2 * kBlock] += quant(w);
       if constexpr (kTrace) pd_trunc += w;
       finish(2);
       return;
     }
+    if constexpr (!kF32) deposit_run();  // FP64: every step is its own deposit
     tf = te;
-    rs = 0.0f;
+    rs = Real(0);
     if constexpr (kGates) {
       if (te >= gate_end && gate_of(te) != gate) deposit_run();  // a new gate closes the run
       set_gate(te);
@@ -314,7 +395,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // flight (checked at setup and after every face, scatter / horizon win ties,
   // transport.cpp:175, 191), so every lane that enters a walk step crosses.
   auto walk = [&]() {
-    const float s = fminf(tmx, fminf(tmy, tmz));
+    const Real s = F::vmin(tmx, F::vmin(tmy, tmz));
     absorb(s);
     if constexpr (kTrace) ++steps;
     deposit_run();  // the voxel left behind
@@ -346,64 +427,75 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         L = s;
         fax = a0 ? 0 : (a1 ? 1 : 2);
       }
-    } else if (fminf(tmx, fminf(tmy, tmz)) >= fabsf(L)) {
+    } else if (F::vmin(tmx, F::vmin(tmy, tmz)) >= F::vabs(L)) {
       phase = ENDF;  // the flight ends in this voxel
     }
   };
 
   // ---- hg_scatter + new free path + roulette (transport.cpp:126-147, 14-17, 333-343) ----
   auto scatter = [&]() {
-    const Medium<float>& M = medium(lab);
+    const Medium<Real>& M = medium(lab);
     if (phase == SCAT) {  // Henyey-Greenstein cos(theta) (transport.cpp:120-124)
       if constexpr (kTrace || kDet) ++nscat;
-      const float xi = rng.template unit<float>();
-      float ct;
+      const Real xi = rng.template unit<Real>();
+      Real ct;
       if (M.iso) {
-        ct = 2.0f * xi - 1.0f;
-      } else {
+        ct = Real(2) * xi - Real(1);
+      } else if constexpr (kF32) {
         const float f = M.hg_c * Tr::rcp(M.hg_d + M.hg_e * xi);
         ct = fminf(1.0f, fmaxf(-1.0f, M.hg_a - f * f * M.hg_b));
+      } else {
+        const double g = M.g;
+        const double tmp = (1.0 - g * g) / (1.0 - g + 2.0 * g * xi);
+        ct = (1.0 + g * g - tmp * tmp) / (2.0 * g);
+        ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
       }
       sct = ct;
-      sst = Tr::sqrt_(fmaxf(0.0f, 1.0f - ct * ct));
+      sst = Tr::sqrt_(F::vmax(Real(0), Real(1) - ct * ct));
     }
     // rejection azimuth (transport.cpp:32-44), VMC_AZ_UNROLL tries per event
     // phase; a lane rejected every time keeps cos/sin(theta) and retries in the
     // next event phase
-    float ax_ = 0, ay_ = 0, r2 = 0;
+    Real ax_ = 0, ay_ = 0, r2 = 0;
     bool ok = false;
 #pragma unroll
     for (int k = 0; k < VMC_AZ_UNROLL; ++k) {
       if (k == 0 || !ok) {
-        ax_ = fmaf(rng.u24(), 0x1p-23f, -1.0f);  // 2u - 1, exact
-        ay_ = fmaf(rng.u24(), 0x1p-23f, -1.0f);
+        ax_ = F::two_u_m1(rng);  // 2u - 1
+        ay_ = F::two_u_m1(rng);
         r2 = ax_ * ax_ + ay_ * ay_;
-        ok = r2 > 1e-12f && r2 <= 1.0f;
+        ok = r2 > Real(1e-12) && r2 <= Real(1);
       }
     }
     if (!ok) {
       phase = RETRY;
       return;
     }
-    const float k = Tr::rsqrt(r2);
-    const float cp = ax_ * k, sp = ay_ * k;
-    const float ct = sct, st = sst;
-    float ox, oy, oz;
-    if (fabsf(dz) > 0.99999f) {  // transport.cpp:133-136
+    const Real k = Tr::rsqrt(r2);
+    const Real cp = ax_ * k, sp = ay_ * k;
+    const Real ct = sct, st = sst;
+    Real ox, oy, oz;
+    if (F::vabs(dz) > Real(0.99999)) {  // transport.cpp:133-136
       ox = st * cp;
       oy = st * sp;
-      oz = dz > 0.0f ? ct : -ct;
-    } else {
+      oz = dz > Real(0) ? ct : -ct;
+    } else if constexpr (kF32) {
       const float one_m = 1.0f - dz * dz;
       const float rden = Tr::rsqrt(one_m);
       const float sr = st * rden;
       ox = sr * (dx * dz * cp - dy * sp) + dx * ct;
       oy = sr * (dy * dz * cp + dx * sp) + dy * ct;
       oz = -st * cp * (one_m * rden) + dz * ct;
+    } else {  // transport.cpp:137-141
+      const double den = sqrt(1.0 - dz * dz);
+      ox = st * (dx * dz * cp - dy * sp) / den + dx * ct;
+      oy = st * (dy * dz * cp + dx * sp) / den + dy * ct;
+      oz = -st * cp * den + dz * ct;
     }
-    const float n2 = ox * ox + oy * oy + oz * oz;  // renormalize (1e-6 in FP32)
-    if (fabsf(n2 - 1.0f) > 1e-6f) {
-      const float kk = Tr::rsqrt(n2);
+    // renormalize (transport.cpp:142-145; 1e-6 in FP32, the reference's 1e-12 in FP64)
+    const Real n2 = ox * ox + oy * oy + oz * oz;
+    if (F::vabs(n2 - Real(1)) > (kF32 ? Real(1e-6) : Real(1e-12))) {
+      const Real kk = Tr::rsqrt(n2);
       ox *= kk;
       oy *= kk;
       oz *= kk;
@@ -413,8 +505,8 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     dz = oz;
     rs = scat_len();
     phase = SETUP;
-    if (w < A.rthrf) {  // roulette after a scatter only (transport.cpp:300-306)
-      const bool survive = rng.template unit<float>() < A.inv_rmultf;
+    if (w < F::pick(A.rthrf, A.rthr)) {  // roulette after a scatter only (transport.cpp:300-306)
+      const bool survive = rng.template unit<Real>() < F::pick(A.inv_rmultf, A.inv_rmult);
       deposit_run();  // close the deposit run before the weight jumps
       const long long qb = quant(w);
       if constexpr (kTrace) pd_kill += w;
@@ -423,7 +515,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         finish(1);
         return;
       }
-      w *= A.rmultf;
+      w *= F::pick(A.rmultf, static_cast<double>(A.rmult));
       acc_sm[kBlock] += qb - quant(w);
       if constexpr (kTrace) pd_kill -= w;
       run_w0 = w;
@@ -432,22 +524,22 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
 
   // ---- interface / exterior face at distance L (handle_interface, transport.cpp:227-298) ----
   auto face = [&]() {
-    const float s = L;
+    const Real s = L;
     const int ax = fax;
-    const float t = tf + s * nsmm_();
+    const Real t = tf + s * nsmm_();
     {
       // land exactly on the crossed plane (transport.cpp:197-204); the voxel
       // index has already moved, so the plane is its near face
       const int u = ax == 0 ? vx : (ax == 1 ? vy : vz);
-      const float dax = ax == 0 ? dx : (ax == 1 ? dy : dz);
-      const float plane = static_cast<float>(dax > 0.0f ? u : u + 1) * h;
+      const Real dax = ax == 0 ? dx : (ax == 1 ? dy : dz);
+      const Real plane = static_cast<Real>(dax > Real(0) ? u : u + 1) * h;
       px = ax == 0 ? plane : px + dx * s;
       py = ax == 1 ? plane : py + dy * s;
       pz = ax == 2 ? plane : pz + dz * s;
     }
     add_path(s);
-    const Medium<float>& M = medium(lab);
-    rs = fmaxf(0.0f, rs - s * M.mus);
+    const Medium<Real>& M = medium(lab);
+    rs = F::vmax(Real(0), rs - s * M.mus);
     const bool ext = static_cast<unsigned>(vx) >= static_cast<unsigned>(nx) ||
                      static_cast<unsigned>(vy) >= static_cast<unsigned>(ny) ||
                      static_cast<unsigned>(vz) >= static_cast<unsigned>(nz);
@@ -460,29 +552,41 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       if (c1 == c2) {
         exited = ext;  // n1 == n2: identity interface / same-n move (:218-223, 242-252)
       } else {
-        const float dax = ax == 0 ? dx : (ax == 1 ? dy : dz);
-        const float n1 = M.n, n2 = sm_media[nl].n;
-        const float ci = fabsf(dax);
-        const float si2 = fmaxf(0.0f, 1.0f - ci * ci);
-        // MUFU reciprocal / sqrt: R only meets a 24-bit uniform, and the
+        const Real dax = ax == 0 ? dx : (ax == 1 ? dy : dz);
+        const Real n1 = M.n, n2 = sm_media[nl].n;
+        const Real ci = F::vabs(dax);
+        const Real si2 = F::vmax(Real(0), Real(1) - ci * ci);
+        // FP32: MUFU reciprocal / sqrt: R only meets a 24-bit uniform, and the
         // interface code runs on few lanes at a time, so its length is its cost
-        const float eta = n1 * Tr::rcp(n2);
-        const float st2 = eta * eta * si2;
-        if (st2 > 1.0f) {
+        Real eta;
+        if constexpr (kF32) {
+          eta = n1 * Tr::rcp(n2);
+        } else {
+          eta = n1 / n2;
+        }
+        const Real st2 = eta * eta * si2;
+        if (st2 > Real(1)) {
           back = true;  // total internal reflection: deterministic flip
         } else {
-          const float cost = Tr::sqrt_(1.0f - st2);
-          const float rsp = (n1 * ci - n2 * cost) * Tr::rcp(n1 * ci + n2 * cost);
-          const float rpp = (n1 * cost - n2 * ci) * Tr::rcp(n1 * cost + n2 * ci);
-          const float R = 0.5f * (rsp * rsp + rpp * rpp);
-          if (rng.template unit<float>() < R) {
+          const Real cost = Tr::sqrt_(Real(1) - st2);
+          Real R;
+          if constexpr (kF32) {
+            const float rsp = (n1 * ci - n2 * cost) * Tr::rcp(n1 * ci + n2 * cost);
+            const float rpp = (n1 * cost - n2 * ci) * Tr::rcp(n1 * cost + n2 * ci);
+            R = 0.5f * (rsp * rsp + rpp * rpp);
+          } else {
+            const double rsp = (n1 * ci - n2 * cost) / (n1 * ci + n2 * cost);
+            const double rpp = (n1 * cost - n2 * ci) / (n1 * cost + n2 * ci);
+            R = 0.5 * (rsp * rsp + rpp * rpp);
+          }
+          if (rng.template unit<Real>() < R) {
             back = true;
           } else {  // Snell refraction, tangential components scaled by n1/n2
-            const float nc = dax > 0.0f ? cost : -cost;
-            const float qx = ax == 0 ? nc : dx * eta;
-            const float qy = ax == 1 ? nc : dy * eta;
-            const float qz = ax == 2 ? nc : dz * eta;
-            const float k = Tr::rsqrt(qx * qx + qy * qy + qz * qz);
+            const Real nc = dax > Real(0) ? cost : -cost;
+            const Real qx = ax == 0 ? nc : dx * eta;
+            const Real qy = ax == 1 ? nc : dy * eta;
+            const Real qz = ax == 2 ? nc : dz * eta;
+            const Real k = Tr::rsqrt(qx * qx + qy * qy + qz * qz);
             dx = qx * k;
             dy = qy * k;
             dz = qz * k;
@@ -497,9 +601,17 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       if constexpr (kDet) {
         int hit = -1;
         for (int k = 0; k < A.ndet; ++k) {
-          // FP32 like the exit position itself (detf = {x, y, z, r^2})
-          const float ex = px - A.detf[k][0], ey = py - A.detf[k][1], ez = pz - A.detf[k][2];
-          if (ex * ex + ey * ey + ez * ez <= A.detf[k][3]) {
+          // in the kernel's precision, like the exit position itself
+          // (FP32: detf = {x, y, z, r^2})
+          bool in;
+          if constexpr (kF32) {
+            const float ex = px - A.detf[k][0], ey = py - A.detf[k][1], ez = pz - A.detf[k][2];
+            in = ex * ex + ey * ey + ez * ez <= A.detf[k][3];
+          } else {
+            const double ex = px - A.det[k][0], ey = py - A.det[k][1], ez = pz - A.det[k][2];
+            in = ex * ex + ey * ey + ez * ez <= A.det[k][3] * A.det[k][3];
+          }
+          if (in) {
             hit = k;
             break;
           }
@@ -520,11 +632,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
               hd.photon_index = idx;
               hd.det_id = static_cast<uint32_t>(hit);
               hd.nscat = nscat;
-              hd.w_exit = w;
-              hd.t_exit_ns = t;
+              hd.w_exit = static_cast<float>(w);
+              hd.t_exit_ns = static_cast<float>(t);
               *reinterpret_cast<vmc_det_record_head*>(rec) = hd;
               float* pp = reinterpret_cast<float*>(rec + sizeof(vmc_det_record_head));
-              for (int m = 0; m < A.nppath; ++m) pp[m] = pp_sm[m * kBlock];
+              for (int m = 0; m < A.nppath; ++m) pp[m] = static_cast<float>(pp_sm[m * kBlock]);
             }
           }
         }
@@ -555,11 +667,16 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   auto launch = [&]() {
     int ux, uy, uz;
     if (A.iso_source) {
-      const float ct = 2.0f * rng.template unit<float>() - 1.0f;
-      const float u2 = rng.template unit<float>();
-      float st, cphi, sphi;
-      st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
-      sincospif(2.0f * u2, &sphi, &cphi);
+      const Real ct = Real(2) * rng.template unit<Real>() - Real(1);
+      const Real u2 = rng.template unit<Real>();
+      Real st, cphi, sphi;
+      if constexpr (kF32) {
+        st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+        sincospif(2.0f * u2, &sphi, &cphi);
+      } else {
+        st = sqrt(fmax(0.0, 1.0 - ct * ct));
+        sincos(2.0 * 3.14159265358979323846 * u2, &sphi, &cphi);
+      }
       dx = st * cphi;
       dy = st * sphi;
       dz = ct;
@@ -570,23 +687,23 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       ux = static_cast<int>(floor(qx / A.h));
       uy = static_cast<int>(floor(qy / A.h));
       uz = static_cast<int>(floor(qz / A.h));
-      px = static_cast<float>(qx);
-      py = static_cast<float>(qy);
-      pz = static_cast<float>(qz);
+      px = static_cast<Real>(qx);
+      py = static_cast<Real>(qy);
+      pz = static_cast<Real>(qz);
       if (ux < 0 || uy < 0 || uz < 0 || ux >= nx || uy >= A.ny || uz >= A.nz) {
         atomicExch(A.error_flag, 1);
         ux = uy = uz = 0;
-        dx = dy = 0.0f;
-        dz = 1.0f;
+        dx = dy = Real(0);
+        dz = Real(1);
       }
       lab = __ldg(A.labels + (ux + nx * (uy + static_cast<long long>(A.ny) * uz)));
     } else {
-      dx = static_cast<float>(A.dir0[0]);
-      dy = static_cast<float>(A.dir0[1]);
-      dz = static_cast<float>(A.dir0[2]);
-      px = static_cast<float>(A.pos0[0]);
-      py = static_cast<float>(A.pos0[1]);
-      pz = static_cast<float>(A.pos0[2]);
+      dx = static_cast<Real>(A.dir0[0]);
+      dy = static_cast<Real>(A.dir0[1]);
+      dz = static_cast<Real>(A.dir0[2]);
+      px = static_cast<Real>(A.pos0[0]);
+      py = static_cast<Real>(A.pos0[1]);
+      pz = static_cast<Real>(A.pos0[2]);
       ux = A.v0[0];
       uy = A.v0[1];
       uz = A.v0[2];
@@ -595,14 +712,14 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     vx = ux;
     vy = uy;
     vz = uz;
-    w = 1.0f;
-    tf = 0.0f;
-    run_w0 = 1.0f;
+    w = Real(1);
+    tf = Real(0);
+    run_w0 = Real(1);
     if (A.iso_source) rs = scat_len();  // pencil: drawn in the seed batch
     if constexpr (kGates) {
       gate = 0;
       gmap = cbase;
-      gate_end = A.ngates > 1 ? A.gate_wf : Tr::inf();
+      gate_end = A.ngates > 1 ? F::pick(A.gate_wf, A.tmax / A.ngates) : Tr::inf();
     }
     if constexpr (kTrace) {
       steps = nscat = 0;
@@ -610,7 +727,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
     if constexpr (kDet) {
       nscat = 0;
-      for (int m = 0; m < A.nppath; ++m) pp_sm[m * kBlock] = 0.0f;
+      for (int m = 0; m < A.nppath; ++m) pp_sm[m * kBlock] = Real(0);
     }
     phase = SETUP;
   };
@@ -619,11 +736,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   // st_base + 0..31 and a header {next unused slot, valid slots}; st_base and
   // st_claimed_all are warp-uniform registers
   const int warp = threadIdx.x >> 5;
-  unsigned char* const stash = smem + kStashOff + warp * (32 * 20 + 16);
+  unsigned char* const stash = smem + kStashOff + warp * kStashBytes;
   uint64_t* const st_a = reinterpret_cast<uint64_t*>(stash);
   uint64_t* const st_b = st_a + 32;
-  float* const st_rs = reinterpret_cast<float*>(stash + 32 * 16);  // pencil sources: first free path
-  int* const st_hdr = reinterpret_cast<int*>(stash + 32 * 16 + 32 * 4);
+  Real* const st_rs = reinterpret_cast<Real*>(stash + 32 * 16);  // pencil sources: first free path
+  int* const st_hdr = reinterpret_cast<int*>(stash + 32 * 16 + 32 * static_cast<int>(sizeof(Real)));
   if (lane == 0) st_hdr[0] = st_hdr[1] = 0;
   __syncwarp();
   unsigned long long st_base = 0;
@@ -676,7 +793,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
           if (lane < nvalid) {
             Rng sr;
             sr.seed(A.seed, A.first + base + lane);
-            if (!A.iso_source) st_rs[lane] = scat_len_of(sr);  // a pencil's first draw (transport.cpp:105)
+            if (!A.iso_source) st_rs[lane] = F::scat_len(sr);  // a pencil's first draw (transport.cpp:105)
             st_a[lane] = sr.a;
             st_b[lane] = sr.b;
           }

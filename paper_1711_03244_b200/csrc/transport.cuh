@@ -49,6 +49,11 @@ constexpr int kMaxDet = 16;
 constexpr int kMaxDetMedia = 8;
 constexpr double kLightMmPerNs = 299.792458;  // types.hpp:16
 
+// K1f per-warp seed stash: 32 x {u64 a, u64 b}, 32 first free paths (Real), header
+__host__ __device__ constexpr int flight_stash_bytes(unsigned long real_bytes) {
+  return static_cast<int>(32 * 16 + 32 * real_bytes + 16);
+}
+
 // Per-label optical data, staged in shared memory at CTA start.
 template <typename Real>
 struct alignas(16) Medium {

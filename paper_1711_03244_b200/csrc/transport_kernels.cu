@@ -3,9 +3,7 @@
 // the product path) and once with -DVMC_REAL=double --fmad=false (parity mode;
 // no contraction, like the reference built with -ffp-contract=off).
 #include "transport.cuh"
-#if VMC_REAL_IS_FLOAT
 #include "flight.cuh"
-#endif
 
 #ifndef VMC_REAL
 #define VMC_REAL float
@@ -60,34 +58,56 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
   }
 }
 
-#if VMC_REAL_IS_FLOAT
-// K1f (flight.cuh): the FP32 product kernel. Same register cap as K1.
-template <bool G, bool D, bool T, bool U, int Abs = -1>
+// K1f (flight.cuh). FP32: the product kernel, same register cap as K1.
+// FP64 (--fmad=false): the exact-arithmetic pin of the same flight structure.
+template <typename R, bool G, bool D, bool T, bool U, int Abs = -1>
 __global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const __grid_constant__ KernelArgs A) {
-  flight_body<G, D, T, U, Abs>(A);
+  flight_body<R, G, D, T, U, Abs>(A);
 }
 
+#if VMC_REAL_IS_FLOAT
 // absorb_mode: the launch's KernelArgs::absorb_mode; the BASELINE workloads'
 // production variants are compiled for their mode (see flight_body's kAbs)
 const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode) {
+  using R = float;
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
-  if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<false, false, false, true, 0>);
-  if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<false, true, false, false, 0>);
-  if (absorb_mode == 1 && !uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<true, false, false, false, 1>);
+  if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, 0>);
+  if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, 0>);
+  if (absorb_mode == 1 && !uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false, 1>);
 #define VMC_FK(k, U)                                                                     \
   case k:                                                                                \
-    return reinterpret_cast<const void*>(&k_flight<(k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);
+    return reinterpret_cast<const void*>(&k_flight<R, (k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);
   if (uniform) {
     switch (key) {
       VMC_FK(0, true) VMC_FK(1, true) VMC_FK(2, true) VMC_FK(3, true)
-      VMC_FK(4, true) VMC_FK(5, true) VMC_FK(6, true) default: return reinterpret_cast<const void*>(&k_flight<true, true, true, true>);
+      VMC_FK(4, true) VMC_FK(5, true) VMC_FK(6, true) default: return reinterpret_cast<const void*>(&k_flight<R, true, true, true, true>);
     }
   }
   switch (key) {
     VMC_FK(0, false) VMC_FK(1, false) VMC_FK(2, false) VMC_FK(3, false)
-    VMC_FK(4, false) VMC_FK(5, false) VMC_FK(6, false) default: return reinterpret_cast<const void*>(&k_flight<true, true, true, false>);
+    VMC_FK(4, false) VMC_FK(5, false) VMC_FK(6, false) default: return reinterpret_cast<const void*>(&k_flight<R, true, true, true, false>);
   }
 #undef VMC_FK
+}
+#else
+// FP64 K1f: the single-label specialisation only for the plain and gated
+// variants (as K1); absorb is always the reference's exp_neg
+const void* flight_kernel_double(bool gates, bool det, bool trace, bool uniform) {
+  using R = double;
+  if (uniform && !det && !trace)
+    return gates ? reinterpret_cast<const void*>(&k_flight<R, true, false, false, true>)
+                 : reinterpret_cast<const void*>(&k_flight<R, false, false, false, true>);
+  const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
+  switch (key) {
+    case 0: return reinterpret_cast<const void*>(&k_flight<R, false, false, false, false>);
+    case 1: return reinterpret_cast<const void*>(&k_flight<R, false, false, true, false>);
+    case 2: return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false>);
+    case 3: return reinterpret_cast<const void*>(&k_flight<R, false, true, true, false>);
+    case 4: return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false>);
+    case 5: return reinterpret_cast<const void*>(&k_flight<R, true, false, true, false>);
+    case 6: return reinterpret_cast<const void*>(&k_flight<R, true, true, false, false>);
+    default: return reinterpret_cast<const void*>(&k_flight<R, true, true, true, false>);
+  }
 }
 #endif
 

@@ -478,6 +478,16 @@ class Plan:
     def launches_per_run(self) -> int:
         return int(lib().vmc_plan_launches_per_run(self._h, 0))
 
+    @property
+    def kernel_name(self) -> str:
+        """Mangled symbol of the transport kernel variant this plan launches."""
+        return (lib().vmc_plan_kernel_name(self._h) or b"").decode()
+
+    @property
+    def kernel(self) -> str:
+        """Readable variant key: 'k_flight<float,G,D,T,U,Abs>' (or k_transport<...>)."""
+        return demangle_kernel(self.kernel_name)
+
     def close(self) -> None:
         if self._h:
             lib().vmc_plan_destroy(self._h)
@@ -488,6 +498,19 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def demangle_kernel(mangled: str) -> str:
+    """_ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi1EEEvNS_10KernelArgsE -> k_flight<float,1,0,0,0,1>
+    (the two kernel templates' Itanium manglings, decoded without c++filt)."""
+    import re
+    m = re.match(r"_ZN3vmc(\d+)(k_flight|k_transport)I([fd])((?:L[bi]n?\d+E)+)E", mangled or "")
+    if not m:
+        return mangled or ""
+    args = ["float" if m.group(3) == "f" else "double"]
+    for kind, neg, val in re.findall(r"L([bi])(n?)(\d+)E", m.group(4)):
+        args.append(("-" if neg else "") + val)
+    return f"{m.group(2)}<{','.join(args)}>"
 
 
 def trace_photons(scene: Scene, config: SimulationConfig, first: int, count: int,

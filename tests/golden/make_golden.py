@@ -58,16 +58,20 @@ def main():
 
     # BASELINE workloads at N = 2e5 (seed 1): run-level numbers + the map
     # summary used by the GPU gates (absorbed fraction, voxels with >= 100 deposits)
+    # plus the head at its production size (256^3, 10 gates; 5e4 photons) and
+    # B1 at BASELINE's own photon count (1e6)
     work = {}
-    for name in ["b1", "b2", "b3", "head64"]:
+    for name, n in [("b1", 200_000), ("b2", 200_000), ("b3", 200_000), ("head64", 200_000),
+                    ("head256", 50_000), ("b1_1e6", 1_000_000)]:
         if name == "head64":
-            st = S.baseline_setup("head", photons=200_000, head_n=64)
+            st = S.baseline_setup("head", photons=n, head_n=64)
+        elif name == "head256":
+            st = S.baseline_setup("head", photons=n, head_n=256)
         else:
-            st = S.baseline_setup(name, photons=200_000)
-        w = R.walk(st.scene, st.config, 0, 200_000, threads=os.cpu_count() or 8, cells=True,
+            st = S.baseline_setup(name.split("_")[0], photons=n)
+        w = R.walk(st.scene, st.config, 0, n, threads=os.cpu_count() or 8, cells=True,
                    counts=True, traces=False, detectors=bool(st.config.detectors))
-        cw = w["cells"].reshape(st.config.ngates, -1).sum(axis=0)
-        rec = {"photons": 200_000, "disp": w["disp"], "raw_sum": int(w["cells"].sum()),
+        rec = {"photons": n, "disp": w["disp"], "raw_sum": int(w["cells"].sum()),
                "gate_sums": [int(x) for x in w["cells"].reshape(st.config.ngates, -1).sum(axis=1)],
                "voxels_ge100": int((w["counts"] >= 100).sum())}
         if "det_count" in w:

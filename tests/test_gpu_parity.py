@@ -41,12 +41,32 @@ def test_rng_kat_device(gpu, golden, ref):
     assert gpu.rng_kat(7, 99, 5000) == ref.rng_kat(7, 99, 5000)[0]
 
 
-@pytest.mark.parametrize("name,thr", [("b1", 0.999), ("b2", 0.999), ("b3", 0.999)])
-def test_fp64_per_photon(gpu, ref, name, thr):
+def _use_kernel(monkeypatch, kernel):
+    """kernel: "flight" = K1f (the product kernel's structure, default), "step" = K1."""
+    if kernel == "step":
+        monkeypatch.setenv("VMC_KERNEL", "step")
+    else:
+        monkeypatch.delenv("VMC_KERNEL", raising=False)
+
+
+@pytest.mark.parametrize("kernel", ["flight", "step"])
+@pytest.mark.parametrize("name,thr", [("b1", 0.999), ("b2", 0.999), ("b3", 0.999), ("head64", 0.999)])
+def test_fp64_per_photon(gpu, ref, monkeypatch, kernel, name, thr):
+    """FP64 mode, photon by photon against the compiled reference. kernel=flight
+    is the FP64 instantiation of K1f (flight_body<double>, --fmad=false): the
+    product kernel's flight decomposition, warp event phases and seed stash
+    with the reference's arithmetic, so any discrete-logic slip in K1f shows
+    up here as a draw-count or disposition mismatch."""
+    _use_kernel(monkeypatch, kernel)
     st = setup(name)
     st.config.precision = v.Precision.FP64
-    tr = gpu.trace_photons(st.scene, st.config, 0, 20_000)
-    rt = ref.walk(st.scene, st.config, 0, 20_000, threads=8, cells=False, traces=True)["traces"]
+    n = 5_000 if name == "head64" else 20_000
+    p = gpu.Plan(st.scene, st.config)
+    want = "k_flight<double" if kernel == "flight" else "k_transport<double"
+    assert p.kernel.startswith(want), p.kernel
+    tr = p.trace(0, n)
+    p.close()
+    rt = ref.walk(st.scene, st.config, 0, n, threads=8, cells=False, traces=True)["traces"]
     same = tr["draws"] == rt["draws"]
     assert same.mean() >= thr
     # a photon can keep its draw count yet flip a Fresnel decision (both branches
@@ -107,8 +127,10 @@ def test_run_parity(gpu, ref, golden, name, tol):
         assert np.all(np.abs(gs[big] / rs[big] - 1) < 0.02)
 
 
-def test_fp64_run_parity(gpu, ref):
+@pytest.mark.parametrize("kernel", ["flight", "step"])
+def test_fp64_run_parity(gpu, ref, monkeypatch, kernel):
     import oracle
+    _use_kernel(monkeypatch, kernel)
     st = setup("b2", n=100_000)
     st.config.precision = v.Precision.FP64
     g = gpu.run_group_dynamic(0, 100_000, 1, st.scene, st.config)
@@ -331,8 +353,10 @@ def test_corner_fp32_per_photon(gpu, ref, kind):
     assert np.abs(books - 1.0).max() < 1e-5
 
 
+@pytest.mark.parametrize("kernel", ["flight", "step"])
 @pytest.mark.parametrize("kind", CORNERS)
-def test_corner_fp64_per_photon(gpu, ref, kind):
+def test_corner_fp64_per_photon(gpu, ref, monkeypatch, kernel, kind):
+    _use_kernel(monkeypatch, kernel)
     scene, cfg = _corner_scene(kind)
     cfg.precision = v.Precision.FP64
     tr = gpu.trace_photons(scene, cfg, 0, 5000)
