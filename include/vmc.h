@@ -206,7 +206,9 @@ VMC_API uint64_t vmc_plan_cell_count(const vmc_plan* plan);
  * legacy default). Device buffers: d_cells [cell_count] int64 (accumulated),
  * d_totals [4] int64 (deposited/escaped/killed/truncated quanta, accumulated),
  * d_det (det_capacity records) and d_det_count [1] uint64 (may be NULL when
- * ndet == 0). Asynchronous: returns after enqueueing. */
+ * ndet == 0). Asynchronous: returns after enqueueing. Runs of one plan share
+ * its claim counter and scratch maps, so each run is ordered after the
+ * previous run of the same plan even across streams (an event wait). */
 VMC_API int vmc_plan_run(vmc_plan* plan, uint64_t first_index, uint64_t count, int64_t* d_cells,
                  int64_t* d_totals, void* d_det, uint64_t* d_det_count, void* stream,
                  uint32_t flags);
@@ -225,6 +227,15 @@ VMC_API int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t 
 
 /* FNV-1a 64 of a byte buffer (the reference's volume checksum, volume_io.cpp:13-20). Host only. */
 VMC_API uint64_t vmc_fnv1a64(const void* data, size_t bytes);
+
+/* Sorts n detector records written by vmc_plan_run for photons
+ * [first_index, first_index+count) by photon index into d_out (device, n
+ * records, must not alias d_recs), on `stream`. Records of contiguous ranges
+ * sorted this way and concatenated in range order are globally sorted, which
+ * is how multi-GPU gathers stay identical for any GPU count. Requires
+ * count <= 2^32. Asynchronous. */
+VMC_API int vmc_plan_sort_records(vmc_plan* plan, const void* d_recs, uint64_t n, uint64_t first_index,
+                                  uint64_t count, void* d_out, void* stream);
 
 /* Mangled device symbol of the transport kernel variant this plan launches
  * (e.g. _ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi1EEEvNS_10KernelArgsE = the FP32

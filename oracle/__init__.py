@@ -98,7 +98,13 @@ class RefLib(_Base):
         lib.ref_fresnel.restype = C.c_double
         lib.ref_fresnel.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.ref_distance_to_boundary.argtypes = [S, P(C.c_double), P(C.c_double), P(C.c_double)]
+        self.has_pipeline = hasattr(lib, "ref_run_pipeline")
+        if self.has_pipeline:
+            lib.ref_run_pipeline.argtypes = [S, Cf, C.c_int, P(C.c_double), P(C.c_double), P(C.c_double)]
+            lib.ref_normalize.argtypes = [S, u64, vp, C.c_int, vp]
         self.lib = lib
+        self.path = path
+        self.build = os.path.basename(path)
 
     def _ck(self, rc):
         self._check(rc, self.lib.ref_last_error)
@@ -123,6 +129,36 @@ class RefLib(_Base):
                                         cells.ctypes.data if cells is not None else None, disp,
                                         C.byref(wall)))
         return cells, list(disp), wall.value
+
+    def run_pipeline(self, scene: Scene, config: SimulationConfig, threads: int = 0):
+        """voxmc::run_pipeline over photons [0, config.photon_count) with the
+        default roster host_device(threads) (0 = all hardware threads).
+        Returns (makespan_ms, e2e_ms, total deposited weight)."""
+        m = Marshalled(scene, config)
+        mk, e2e = C.c_double(), C.c_double()
+        disp = (C.c_double * 4)()
+        self._ck(self.lib.ref_run_pipeline(C.byref(m.scene), C.byref(m.config), threads, C.byref(mk),
+                                           C.byref(e2e), disp))
+        return mk.value, e2e.value, disp[0]
+
+    def time_pipeline(self, scene, config, n: int, threads: int) -> float:
+        """ms of run_pipeline over n photons (RunReport::makespan_ms, config.cpp:305)."""
+        import copy
+        cfg = copy.copy(config)
+        cfg.photon_count = n
+        return self.run_pipeline(scene, cfg, threads)[0]
+
+    def time_group(self, scene, config, n: int, threads: int) -> float:
+        return self.run_group(scene, config, 0, n, threads, want_cells=False)[2]
+
+    def normalize(self, scene: Scene, photon_count: int, cells: np.ndarray, normalized: bool = True):
+        """FluenceMap::normalize + to_float_volume of raw cells (fluence.cpp:62-90)."""
+        c = np.ascontiguousarray(cells, dtype=np.int64).reshape(-1)
+        out = np.empty(scene.grid.voxel_count, np.float32)
+        m = Marshalled(scene, SimulationConfig(photon_count=photon_count))
+        self._ck(self.lib.ref_normalize(C.byref(m.scene), photon_count, c.ctypes.data, 1 if normalized else 0,
+                                        out.ctypes.data))
+        return out
 
     def run_multi(self, scene, config, total, profiles, strategy, threads_per_device=1):
         m = Marshalled(scene, config)
@@ -264,6 +300,66 @@ class COracle(_Base):
 
 _ref_singleton: Optional[RefLib] = None
 _c_singleton: Optional[COracle] = None
+
+
+BENCH_ISAS = ["sapphirerapids", "emeraldrapids", "icelake-server", "znver4", "znver3", "x86-64-v4"]
+
+
+def host_march() -> str:
+    """What `gcc -march=native` resolves to on this host ("" if unknown)."""
+    try:
+        out = subprocess.run(["gcc", "-march=native", "-Q", "--help=target"], capture_output=True, text=True,
+                             timeout=30).stdout
+        for line in out.splitlines():
+            t = line.split()
+            if len(t) == 2 and t[0] == "-march=":
+                return t[1]
+    except Exception:
+        pass
+    return ""
+
+
+def _cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except Exception:
+        pass
+    return set()
+
+
+_best_singleton: Optional[RefLib] = None
+
+
+def ref_best() -> RefLib:
+    """The reference build for the CPU baseline: the per-ISA build matching
+    this host's -march=native (the reference's own flag,
+    proj/core/CMakeLists.txt:18), else x86-64-v4 when the host has AVX-512,
+    else the portable x86-64-v3 test build."""
+    global _best_singleton
+    if _best_singleton is None:
+        march = host_march()
+        cand = []
+        if march in BENCH_ISAS:
+            cand.append(march)
+        if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= _cpu_flags():
+            cand.append("x86-64-v4")
+        lib = None
+        for isa in cand:
+            p = os.path.join(HERE, "_ref", f"libvoxmc_ref_bench_{isa}.so")
+            if os.path.exists(p):
+                lib = RefLib(p)
+                lib.build = f"reference core -O3 -march={isa}" + (
+                    " (== this host's -march=native)" if isa == march else
+                    f" (host -march=native is {march or 'unknown'}; widest prebuilt ISA it supports)")
+                break
+        if lib is None:
+            lib = ref()
+            lib.build = "reference core -O3 -march=x86-64-v3 (portable test build)"
+        _best_singleton = lib
+    return _best_singleton
 
 
 def ref() -> RefLib:

@@ -10,6 +10,10 @@
 //   ref_trace      -> voxmc::simulate_photon_trace (proj/core/src/transport.cpp:368-380)
 //   ref_partition  -> voxmc::make_partition      (proj/core/src/scheduler.cpp:244-251)
 //   ref_rng_kat    -> voxmc::RngStream           (proj/core/include/voxmc/rng.hpp:11-35)
+//   ref_run_pipeline -> voxmc::run_pipeline      (proj/core/src/config.cpp:288-321; the
+//                     reference's own front door, timed as the CPU baseline)
+//   ref_normalize  -> voxmc::FluenceMap::normalize + to_float_volume
+//                     (proj/core/src/fluence.cpp:62-90; the checker of K4)
 // plus ONE derived oracle, ref_walk, for the features the reference lacks
 // (time gates, disk detectors, per-photon RNG draw counts). ref_walk re-drives
 // the reference's public step API (launch / advance / handle_interface /
@@ -30,6 +34,8 @@
 #include <thread>
 #include <vector>
 
+#include "voxmc/config.hpp"
+#include "voxmc/fluence.hpp"
 #include "voxmc/oracles.hpp"
 #include "voxmc/scheduler.hpp"
 #include "voxmc/transport.hpp"
@@ -433,6 +439,51 @@ int ref_brute_force(std::uint64_t total, int ndev, const vmc_device_profile* pro
     const auto r = R::oracles::brute_force_partition(total, devs);
     for (int i = 0; i < ndev; ++i) counts_out[i] = r.partition.counts[i];
     if (makespan) *makespan = r.makespan;
+  });
+}
+
+// run_pipeline with the default roster (one host_device(threads) worker pool;
+// threads = 0 -> std::thread::hardware_concurrency, config.cpp:118-125).
+// Photons [0, config.photon_count). makespan_ms = RunReport::makespan_ms (the
+// pool's wall time, config.cpp:305), e2e_ms = the whole call (map allocation,
+// partition, merge, energy audit) on a steady clock.
+int ref_run_pipeline(const vmc_scene* s, const vmc_config* c, int threads, double* makespan_ms,
+                     double* e2e_ms, double* disp4) {
+  return guarded([&] {
+    R::RunSetup setup{make_scene(s), make_config(c), {}, R::Strategy::S1, "", ""};
+    const auto t0 = std::chrono::steady_clock::now();
+    R::RunResult r = R::run_pipeline(setup, threads);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (makespan_ms) *makespan_ms = r.report.makespan_ms;
+    if (e2e_ms) *e2e_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (disp4) {
+      disp4[0] = r.map.total_deposited();
+      disp4[1] = disp4[2] = disp4[3] = 0.0;
+    }
+  });
+}
+
+// FluenceMap(dims, photon_count) holding raw cells `cells` (set through
+// deposit() in chunks the quantum represents exactly), then normalize(grid)
+// (when `normalized`) and to_float_volume() into out[V].
+int ref_normalize(const vmc_scene* s, std::uint64_t photon_count, const std::int64_t* cells, int normalized,
+                  float* out) {
+  return guarded([&] {
+    const R::Scene scene = make_scene(s);
+    R::FluenceMap map(scene.grid.dims(), photon_count);
+    const double q = map.quantum();
+    const std::int64_t chunk = std::int64_t{1} << 52;  // |chunk| * q and back are exact
+    for (std::size_t i = 0; i < map.voxel_count(); ++i) {
+      std::int64_t c = cells[i];
+      while (c != 0) {
+        const std::int64_t part = c > chunk ? chunk : (c < -chunk ? -chunk : c);
+        map.deposit(i, static_cast<double>(part) * q);
+        c -= part;
+      }
+    }
+    if (normalized) map.normalize(scene.grid);
+    const std::vector<float> v = map.to_float_volume();
+    std::copy(v.begin(), v.end(), out);
   });
 }
 

@@ -111,6 +111,7 @@ EXPORTS = (
     "vmc_plan_cell_count", "vmc_plan_run", "vmc_plan_trace", "vmc_plan_normalize", "vmc_fnv1a64",
     "vmc_plan_launches_per_run",
     "vmc_plan_kernel_name",
+    "vmc_plan_sort_records",
 )
 
 
@@ -141,6 +142,7 @@ def declare(lib: C.CDLL) -> C.CDLL:
         "vmc_plan_trace": (C.c_int, [vp, u64, u64, vp]),
         "vmc_plan_launches_per_run": (C.c_int, [vp, u32]),
         "vmc_plan_kernel_name": (C.c_char_p, [vp]),
+        "vmc_plan_sort_records": (C.c_int, [vp, vp, u64, u64, u64, vp, vp]),
         "vmc_plan_normalize": (C.c_int, [vp, vp, u64, vp, C.c_int, C.c_int, vp]),
         "vmc_fnv1a64": (u64, [vp, C.c_size_t]),
     }

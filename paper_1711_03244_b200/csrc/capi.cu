@@ -297,6 +297,14 @@ struct vmc_plan {
   int nrep = 1;
   bool scratch = false, fold_books_deposited = false;
   DevBuf rep;
+  // runs of one plan share the claim counter and the replica scratch, so each
+  // enqueue waits for the previous one (any stream) to finish with them
+  cudaEvent_t done = nullptr;
+  bool done_valid = false;
+  RecSort rs;  // scratch of vmc_plan_sort_records
+  ~vmc_plan() {
+    if (done) cudaEventDestroy(done);
+  }
 };
 
 namespace {
@@ -351,6 +359,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   get(P->claim, cache ? &cache->claim : nullptr, sizeof(unsigned long long));
   get(P->err, cache ? &cache->err : nullptr, sizeof(int));
   ck(cudaMemset(P->err.p, 0, sizeof(int)), "cudaMemset");
+  ck(cudaEventCreateWithFlags(&P->done, cudaEventDisableTiming), "event");
 
   vmc::KernelArgs& A = P->args;
   std::memset(&A, 0, sizeof A);
@@ -532,6 +541,9 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   if (P->cfg.ndet > 0 && !d_det_count) fail_validation("detector count buffer is required");
   if (first + count < first) fail_validation("photon range overflows");
   ck(cudaSetDevice(P->device), "cudaSetDevice");
+  // serialise with the previous run of this plan (shared claim counter and
+  // replica scratch), whatever stream it was enqueued on
+  if (P->done_valid) ck(cudaStreamWaitEvent(st, P->done, 0), "wait previous run");
   const bool zero = (flags & VMC_RUN_ZERO) != 0;
   if (zero) {
     // with a scratch map the fold overwrites the caller's cells instead
@@ -569,6 +581,8 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
                                         P->fold_books_deposited ? 1 : 0);
     ck(cudaGetLastError(), "fold replicas");
   }
+  ck(cudaEventRecord(P->done, st), "record run");
+  P->done_valid = true;
 }
 
 void check_launch_errors(vmc_plan* P) {
@@ -618,16 +632,23 @@ __global__ void k_rec_gather(const uint32_t* __restrict__ src, uint32_t* __restr
 
 // Sort n records (photon indices in [first, first + count), count <= 2^32) on
 // the device: radix sort of the 32-bit index offsets (only the bits count
-// needs) carrying record positions, then a gather into R.out. Returns R.out.
+// needs) carrying record positions, then a gather into `out` (R.out when
+// null). Returns the sorted records.
 const void* sort_records_device(const void* d_recs, uint64_t n, size_t stride, uint64_t first, uint64_t count,
-                                RecSort& R, int device, cudaStream_t st) {
-  if (n < 2) return d_recs;
+                                RecSort& R, int device, cudaStream_t st, void* out = nullptr) {
+  if (n < 2) {
+    if (out && n) ck(cudaMemcpyAsync(out, d_recs, n * stride, cudaMemcpyDeviceToDevice, st), "copy records");
+    return out && n ? out : d_recs;
+  }
   const uint32_t n32 = static_cast<uint32_t>(n);
   R.k0.ensure(n * 4, device);
   R.k1.ensure(n * 4, device);
   R.v0.ensure(n * 4, device);
   R.v1.ensure(n * 4, device);
-  R.out.ensure(n * stride, device);
+  if (!out) {
+    R.out.ensure(n * stride, device);
+    out = R.out.p;
+  }
   int end_bit = 1;
   while (end_bit < 32 && (count - 1) >> end_bit) ++end_bit;
   auto* k0 = static_cast<uint32_t*>(R.k0.p);
@@ -642,10 +663,10 @@ const void* sort_records_device(const void* d_recs, uint64_t n, size_t stride, u
   ck(cub::DeviceRadixSort::SortPairs(R.tmp.p, tb, k0, k1, v0, v1, static_cast<int>(n32), 0, end_bit, st), "cub sort");
   const uint64_t nwords = n * (stride / 4);
   const int grid = static_cast<int>(std::min<uint64_t>((nwords + 255) / 256, 148ull * 16));
-  k_rec_gather<<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(d_recs), static_cast<uint32_t*>(R.out.p), v1, nwords,
+  k_rec_gather<<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(d_recs), static_cast<uint32_t*>(out), v1, nwords,
                                      static_cast<uint32_t>(stride / 4));
   ck(cudaGetLastError(), "record sort");
-  return R.out.p;
+  return out;
 }
 
 // ---- one device, host buffers ---------------------------------------------
@@ -1223,6 +1244,20 @@ uint64_t vmc_fnv1a64(const void* data, size_t bytes) {
     h *= 0x100000001b3ull;
   }
   return h;
+}
+
+int vmc_plan_sort_records(vmc_plan* plan, const void* d_recs, uint64_t n, uint64_t first_index, uint64_t count,
+                          void* d_out, void* stream) {
+  return guarded([&] {
+    if (!plan) fail_validation("null plan");
+    if (n && (!d_recs || !d_out)) fail_validation("sort_records: null buffer");
+    if (d_recs == d_out && n > 1) fail_validation("sort_records: output must not alias the input");
+    if (count > (1ull << 32) || plan->rec_stride % 4 != 0 || n >= (1ull << 31))
+      fail_validation("sort_records: range wider than 2^32 photons or more than 2^31 records");
+    ck(cudaSetDevice(plan->device), "cudaSetDevice");
+    sort_records_device(d_recs, n, plan->rec_stride, first_index, count, plan->rs, plan->device,
+                        static_cast<cudaStream_t>(stream), d_out);
+  });
 }
 
 const char* vmc_plan_kernel_name(const vmc_plan* plan) { return plan ? plan->kern_name.c_str() : ""; }

@@ -461,6 +461,14 @@ class Plan:
                  det.data_ptr() if det is not None else 0,
                  det_count.data_ptr() if det_count is not None else 0, st.cuda_stream, zero)
 
+    def sort_records_torch(self, det, n: int, first: int, count: int, out, stream=None) -> None:
+        """Sort the first n detector records in `det` (written by run_torch for
+        photons [first, first+count)) by photon index into `out` (uint8 tensors)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(lib().vmc_plan_sort_records(self._h, C.c_void_p(det.data_ptr()), n, first, count,
+                                           C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+
     def trace(self, first: int, count: int) -> np.ndarray:
         out = np.zeros(count, dtype=_abi.trace_dtype())
         _check(lib().vmc_plan_trace(self._h, first, count, out.ctypes.data))

@@ -408,8 +408,15 @@ def test_run_group_distributed_single_process_matches(gpu):
     """distributed.run_group_distributed (plan + reduce + root download) with no
     process group == run_group_dynamic over the same range (integer maps)."""
     from paper_1711_03244_b200.distributed import run_group_distributed
-    st = v.baseline_setup("b2", photons=200_000)
-    cells, tq = run_group_distributed(st.scene, st.config)
+    st = v.baseline_setup("b3", photons=200_000)
+    res = run_group_distributed(st.scene, st.config)
     r = gpu.run_group_dynamic(0, 200_000, 1, st.scene, st.config)
-    assert np.array_equal(cells.reshape(-1), r.map.cells.reshape(-1))
-    assert tuple(tq) == tuple(r.totals_q)
+    assert np.array_equal(res.cells.reshape(-1), r.map.cells.reshape(-1))
+    assert tuple(res.totals_q) == tuple(r.totals_q)
+    assert res.det_count == r.det_count > 0
+    assert np.array_equal(res.detections, r.detections)
+    # a total larger than config.photon_count sets the quantum of the total
+    # (scheduler.cpp:412-413), not of the config's count
+    res2 = run_group_distributed(st.scene, st.config, total=300_000)
+    r2 = gpu.run_group_dynamic(0, 300_000, 1, st.scene, v.baseline_setup("b3", photons=300_000).config)
+    assert np.array_equal(res2.cells.reshape(-1), r2.map.cells.reshape(-1))

@@ -75,3 +75,36 @@ def test_rank_ranges_contiguous():
     prof = [v.DeviceProfile(cores=1, a=1e-6, t0=0.1), v.DeviceProfile(cores=1, a=2e-6, t0=0.0)]
     r = rank_ranges(1_000_000, 2, v.Strategy.S3, prof)
     assert r[0][1] > r[1][1]
+
+
+def _gather_worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1711_03244_b200.distributed import gather_records
+    rec_bytes = 16
+    # rank r holds r + 2 sorted records of its own contiguous range (rank 1: none)
+    n = 0 if rank == 1 else rank + 2
+    recs = torch.zeros(8 * rec_bytes, dtype=torch.uint8)
+    view = recs.view(torch.int64).view(-1, 2)
+    for i in range(n):
+        view[i, 0] = 1000 * rank + i  # photon index
+        view[i, 1] = rank             # payload
+    got, counts = gather_records(recs, n, rec_bytes)
+    if rank == 0:
+        np.save(out_path, got.numpy())
+        assert counts == [0 + 2, 0, 2 + 2][:world]
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_detector_record_gather_in_rank_order(tmp_path):
+    """distributed.gather_records: per-rank sorted records (ragged counts, one
+    rank empty) concatenated on rank 0 in rank order, byte for byte."""
+    out = str(tmp_path / "recs.npy")
+    mp.spawn(_gather_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    got = np.load(out).view(np.int64).reshape(-1, 2)
+    assert got[:, 0].tolist() == [0, 1, 2000, 2001, 2002, 2003]
+    assert got[:, 1].tolist() == [0, 0, 2, 2, 2, 2]
