@@ -73,11 +73,13 @@ def build(verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    # L2 red.add microbenchmark (bench.py's secondary atomic roofline)
-    src = os.path.join(ROOT, "tools", "atomics_bench.cu")
-    exe = os.path.join(OUT_DIR, "atomics_bench")
-    if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(src) > os.path.getmtime(exe)):
-        subprocess.run([NVCC] + ARCH + ["-O3", "-lineinfo", "-o", exe, src], check=True)
+    # L2 red.add microbenchmark (bench.py's secondary atomic roofline) and the
+    # red-counter probe (what ncu's L2 red request counter counts)
+    for tool in ("atomics_bench", "red_counter_probe"):
+        src = os.path.join(ROOT, "tools", tool + ".cu")
+        exe = os.path.join(OUT_DIR, tool)
+        if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(src) > os.path.getmtime(exe)):
+            subprocess.run([NVCC] + ARCH + ["-O3", "-lineinfo", "-o", exe, src], check=True)
     return LIB
 
 

@@ -33,7 +33,7 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode);
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode, int dep);
 const void* flight_kernel_double(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
@@ -291,6 +291,7 @@ struct vmc_plan {
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
   std::string kern_name;  // mangled device symbol of `kern` (cudaFuncGetName)
+  int dep = 0;            // deposit path of `kern` (vmc::kDepDirect / kDepWarp / kDepHotBox)
   // fluence-map scratch: nrep replicas (nrep > 1 for small maps) the transport
   // kernel deposits into, folded into the caller's map after each launch. K1f
   // always deposits into the scratch: the fold also books the deposited channel
@@ -456,8 +457,30 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     // VMC_GENERIC_ABSORB=1 (test hook): the generic variant that picks its
     // absorb series at run time instead of the compiled-in production one
     const int abs_sel = env_int("VMC_GENERIC_ABSORB", 0) ? -1 : A.absorb_mode;
-    P->kern = vmc::flight_kernel_float(gates, det, false, uniform, abs_sel);
-    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, abs_sel);
+    // VMC_DEPOSIT=warp|hotbox: the warp-aggregated / SM-local hot-box deposit
+    // paths (A/B; built for the production variants, direct elsewhere)
+    const char* dp = std::getenv("VMC_DEPOSIT");
+    int dep = vmc::kDepDirect;
+    if (dp && std::strcmp(dp, "warp") == 0) dep = vmc::kDepWarp;
+    if (dp && std::strcmp(dp, "hotbox") == 0 && s->nx >= vmc::kHotBoxN && s->ny >= vmc::kHotBoxN &&
+        s->nz >= vmc::kHotBoxN)
+      dep = vmc::kDepHotBox;
+    P->kern = dep != vmc::kDepDirect ? vmc::flight_kernel_float(gates, det, false, uniform, abs_sel, dep) : nullptr;
+    if (P->kern) {
+      P->dep = dep;
+    } else {
+      P->kern = vmc::flight_kernel_float(gates, det, false, uniform, abs_sel, vmc::kDepDirect);
+    }
+    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, abs_sel, vmc::kDepDirect);
+    if (P->dep == vmc::kDepHotBox) {
+      // 16^3 box around the source voxel, clamped into the grid
+      const int n3[3] = {s->nx, s->ny, s->nz};
+      for (int k = 0; k < 3; ++k) {
+        const double p = s->isotropic ? s->src_pos[k] / s->voxel_mm : static_cast<double>(A.v0[k]);
+        const int c = static_cast<int>(std::floor(p)) - vmc::kHotBoxN / 2;
+        A.hb0[k] = std::max(0, std::min(c, n3[k] - vmc::kHotBoxN));
+      }
+    }
   }
   {
     const char* nm = nullptr;
@@ -472,6 +495,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   P->smem = ((P->smem + 15) & ~static_cast<size_t>(15)) + 3 * vmc::kBlock * sizeof(long long) +
             (vmc::kBlock / 32) * vmc::flight_stash_bytes(f64 ? sizeof(double) : sizeof(float));
   P->smem_trace = P->smem;
+  if (P->dep == vmc::kDepHotBox) P->smem += vmc::kHotBoxBytes;
   ck(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device), "sm count");
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem_trace)),

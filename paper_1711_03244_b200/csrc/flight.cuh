@@ -127,7 +127,25 @@ struct FlightOps<double> {
 // cube60 phantoms) / 1 (< 0.15, the head phantom), which drops the warp-uniform
 // mode tests from every absorb(). The double instantiation always uses the
 // reference's exp_neg.
-template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1>
+//
+// kDep: how a closed deposit run reaches the fluence map (all three give the
+// same integer sums, so bit-identical maps):
+//   kDepDirect  one red.global.add.u64 per run into the CTA's map replica;
+//   kDepWarp    warp-aggregated: lanes of one deposit instruction that hit
+//               the same cell (__match_any_sync) sum their quanta by pointer
+//               jumping along the peer list and the lowest lane issues one
+//               red; a warp whose lanes all hit distinct cells takes the
+//               direct path after one vote;
+//   kDepHotBox  an SM-local accumulator: runs inside a 16^3 box around the
+//               source voxel (36 % of B1's deposits) add into
+//               a per-CTA shared-memory box (u64 as a lo/hi u32 pair with an
+//               exact carry: native ATOMS.ADD instead of a 64-bit CAS loop),
+//               flushed to the map with one red per non-empty cell at CTA
+//               exit (the reference's private-map merge, scheduler.cpp:
+//               268-275,312-314, at CTA granularity). Ungated kernels only.
+// (kDepDirect / kDepWarp / kDepHotBox, kHotBoxN: transport.cuh)
+
+template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1, int kDep = kDepDirect>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Tr = RealTraits<Real>;
   using F = FlightOps<Real>;
@@ -142,8 +160,16 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   constexpr int kAccOff = 0;                                       // 3 x kBlock x int64
   constexpr int kStashOff = kAccOff + 3 * kBlock * 8;              // kBlock / 32 x kStashBytes
   constexpr int kPpOff = kStashOff + (kBlock / 32) * kStashBytes;
-  constexpr int kMediaOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * static_cast<int>(sizeof(Real)) : 0);
+  constexpr int kHbOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * static_cast<int>(sizeof(Real)) : 0);
+  constexpr int kMediaOff = kHbOff + (kDep == kDepHotBox ? kHotBoxBytes : 0);
   static_assert(kStashOff % 16 == 0 && kPpOff % 16 == 0 && kMediaOff % 16 == 0, "smem alignment");
+  static_assert(kDep != kDepHotBox || !kGates, "the hot box serves ungated kernels");
+  constexpr int kHbCells = kHotBoxN * kHotBoxN * kHotBoxN;
+  unsigned* const hb_lo = reinterpret_cast<unsigned*>(smem + kHbOff);
+  unsigned* const hb_hi = hb_lo + kHbCells;
+  if constexpr (kDep == kDepHotBox) {
+    for (int i = threadIdx.x; i < 2 * kHbCells; i += blockDim.x) hb_lo[i] = 0u;
+  }
 
   // ---- shared memory: media table (exterior n is needed even when kUni) ----
   Medium<Real>* sm_media = reinterpret_cast<Medium<Real>*>(smem + kMediaOff);
@@ -263,22 +289,66 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     s0 = s;
   };
   auto cell = [&]() -> int { return vx + nx * vy + nxy * vz; };  // x-fastest linear index (two IMAD)
-  // close the open deposit run at weight w_new: one fixed-point add into the
+  // one fixed-point add of q quanta into the current voxel's cell
+  auto red_cell = [&](unsigned long long q) {
+    // ungated launches index from the parameter-bank base (one IMAD.WIDE),
+    // gated ones from the gate's pointer
+    if constexpr (kGates) {
+      atomicAdd(gmap + cell(), q);
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + cell()), q);
+    }
+  };
+  auto add_quanta = [&](unsigned long long q) {
+    if constexpr (kDep == kDepHotBox) {
+      const unsigned ux = static_cast<unsigned>(vx - A.hb0[0]), uy = static_cast<unsigned>(vy - A.hb0[1]),
+                     uz = static_cast<unsigned>(vz - A.hb0[2]);
+      if ((ux | uy | uz) < static_cast<unsigned>(kHotBoxN)) {
+        const int i = static_cast<int>(ux + kHotBoxN * (uy + kHotBoxN * uz));
+        const unsigned lo = static_cast<unsigned>(q);
+        const unsigned old = atomicAdd(hb_lo + i, lo);
+        const unsigned hi = static_cast<unsigned>(q >> 32) + (old + lo < old ? 1u : 0u);  // exact carry
+        if (hi) atomicAdd(hb_hi + i, hi);
+        return;
+      }
+      red_cell(q);
+    } else if constexpr (kDep == kDepWarp) {
+      const unsigned am = __activemask();
+      const int c = cell();
+      const unsigned peers = __match_any_sync(am, c);
+      if (__all_sync(am, peers == (1u << lane))) {
+        red_cell(q);
+        return;
+      }
+      // suffix sums along each peer list by pointer jumping: after five
+      // rounds every lane holds the sum of itself and the peers above it,
+      // so the lowest peer holds its group's total
+      const unsigned above = peers & (0xfffffffeu << lane);
+      int nxt = above ? __ffs(above) - 1 : -1;
+      unsigned long long v = q;
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        const int src = nxt >= 0 ? nxt : lane;
+        const unsigned long long o = __shfl_sync(am, v, src);
+        const int n2 = __shfl_sync(am, nxt, src);
+        if (nxt >= 0) {
+          v += o;
+          nxt = n2;
+        }
+      }
+      if ((peers & lanemask_lt) == 0) red_cell(v);
+    } else {
+      red_cell(q);
+    }
+  };
+  // close the open deposit run at weight w: one fixed-point add into the
   // voxel the run belongs to (the map is L2-resident for cube60)
   auto deposit_run = [&]() {
     const Real dw = run_w0 - w;
     const long long q = quant(dw);
-    // FP32: q == 0 only if mua == 0; ungated launches index from the
-    // parameter-bank base (one IMAD.WIDE), gated ones from the gate's pointer.
-    // FP64: one run per step; empty steps add nothing (run_photon :325-328)
-    if (kF32 || q != 0) {
-      if constexpr (kGates) {
-        atomicAdd(gmap + cell(), static_cast<unsigned long long>(q));
-      } else {
-        atomicAdd(reinterpret_cast<unsigned long long*>(A.cells) + (roff + cell()),
-                  static_cast<unsigned long long>(q));
-      }
-    }
+    // FP32: q == 0 only if mua == 0. FP64: one run per step; empty steps add
+    // nothing (run_photon :325-328)
+    if (kF32 || q != 0) add_quanta(static_cast<unsigned long long>(q));
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
   };
@@ -859,6 +929,18 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
   }
 
+  if constexpr (kDep == kDepHotBox) {
+    // flush the CTA's hot box: one red per non-empty cell into its replica
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHbCells; i += blockDim.x) {
+      const unsigned long long q = hb_lo[i] | (static_cast<unsigned long long>(hb_hi[i]) << 32);
+      if (q) {
+        const int bx = A.hb0[0] + i % kHotBoxN, by = A.hb0[1] + (i / kHotBoxN) % kHotBoxN,
+                  bz = A.hb0[2] + i / (kHotBoxN * kHotBoxN);
+        atomicAdd(cbase + (bx + nx * by + nxy * bz), q);
+      }
+    }
+  }
   // ---- epilogue: dispositions (warp reduce) ----
   long long acc_esc = acc_sm[0], acc_kill = acc_sm[kBlock], acc_trunc = acc_sm[2 * kBlock];
 #pragma unroll

@@ -49,6 +49,11 @@ constexpr int kMaxDet = 16;
 constexpr int kMaxDetMedia = 8;
 constexpr double kLightMmPerNs = 299.792458;  // types.hpp:16
 
+// K1f deposit paths (flight.cuh, flight_body's kDep) and the hot-box edge
+constexpr int kDepDirect = 0, kDepWarp = 1, kDepHotBox = 2;
+constexpr int kHotBoxN = 16;
+constexpr int kHotBoxBytes = kHotBoxN * kHotBoxN * kHotBoxN * 8;
+
 // K1f per-warp seed stash: 32 x {u64 a, u64 b}, 32 first free paths (Real), header
 __host__ __device__ constexpr int flight_stash_bytes(unsigned long real_bytes) {
   return static_cast<int>(32 * 16 + 32 * real_bytes + 16);
@@ -116,6 +121,8 @@ struct KernelArgs {
   int walk_keep;  // K1f: a full warp walks while more than (32 * (100 - event_pct)) / 100 lanes walk
   int pad10, pad7;
   float detf[kMaxDet][4];  // K1f: detector disks as {x, y, z, r^2} in FP32
+  int hb0[3];              // K1f hot-box deposits: box origin voxel (16^3 box around the source)
+  int pad12;
 };
 
 // ---------------------------------------------------------------------------

@@ -202,6 +202,29 @@ def test_map_replicas_bit_identical(gpu, monkeypatch, name):
         assert x.det_count == runs[0].det_count
 
 
+@pytest.mark.parametrize("name,modes", [("b1", ("warp", "hotbox")), ("b2", ("warp", "hotbox")),
+                                        ("b3", ("warp", "hotbox")), ("head", ("warp",))])
+def test_deposit_paths_bit_identical(gpu, monkeypatch, name, modes):
+    """The warp-aggregated and the SM-local hot-box deposit paths of K1f
+    (VMC_DEPOSIT=warp|hotbox) move only where and when the integer quanta are
+    added: maps, dispositions and detector records equal the direct path's."""
+    st = setup(name, n=300_000)
+    monkeypatch.delenv("VMC_DEPOSIT", raising=False)
+    ref_run = gpu.run_group_dynamic(0, 300_000, 1, st.scene, st.config)
+    for mode in modes:
+        monkeypatch.setenv("VMC_DEPOSIT", mode)
+        p = gpu.Plan(st.scene, st.config)
+        want = {"warp": 1, "hotbox": 2}[mode]
+        assert p.kernel.endswith(f",{want}>"), p.kernel
+        p.close()
+        r = gpu.run_group_dynamic(0, 300_000, 1, st.scene, st.config)
+        assert np.array_equal(r.map.cells, ref_run.map.cells), mode
+        assert r.totals_q == ref_run.totals_q
+        assert r.det_count == ref_run.det_count
+        if ref_run.detections is not None:
+            assert np.array_equal(r.detections, ref_run.detections)
+
+
 def test_run_multi_single_device_equals_range(gpu):
     st = setup("b1", n=100_000)
     devs = [gpu.DeviceProfile(name="gpu0", cores=1, gpu=0)]
