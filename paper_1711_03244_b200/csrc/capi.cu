@@ -303,6 +303,9 @@ struct vmc_plan {
   cudaEvent_t done = nullptr;
   bool done_valid = false;
   RecSort rs;  // scratch of vmc_plan_sort_records
+  DevBuf den;  // K4: (mua * V) * N per label for the photon count den_n
+
+  uint64_t den_n = 0;
   ~vmc_plan() {
     if (done) cudaEventDestroy(done);
   }
@@ -502,6 +505,10 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
      "smem attr");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern, P->block, P->smem), "occupancy");
+  {
+    const int cap = env_int("VMC_CTAS_PER_SM", 0);  // A/B knob: fewer resident CTAs per SM
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+  }
   P->grid = std::max(1, per_sm) * P->sms;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern_trace, P->block, P->smem_trace), "occupancy");
   P->grid_trace = std::max(1, per_sm) * P->sms;
@@ -589,14 +596,16 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   A.det_out = static_cast<unsigned char*>(d_det);
   A.det_count = reinterpret_cast<unsigned long long*>(d_det_count);
   A.trace = d_trace;
-  void* argv[] = {&A};
   // never launch more persistent threads than photons need
   const uint64_t need_blocks = (count + P->block - 1) / P->block;
   const int full = trace ? P->grid_trace : P->grid;
   const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));
-  ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv,
-                      trace ? P->smem_trace : P->smem, st),
-     "launch transport");
+  {
+    void* argv[] = {&A};
+    ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv,
+                        trace ? P->smem_trace : P->smem, st),
+       "launch transport");
+  }
   if (P->scratch) {
     const int fb = static_cast<int>(std::min<uint64_t>((P->ncells + 255) / 256, static_cast<uint64_t>(P->sms) * 8));
     k_fold_replicas<<<fb, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_cells),
@@ -844,12 +853,24 @@ constexpr int kNcclSum = 0;    // ncclSum
 
 namespace {
 // K4: normalize (fluence.cpp:62-90). HBM-streaming pass: each thread handles a
-// PAIR of consecutive voxels (16-byte int64x2 loads, 8-byte float2 stores),
-// computes the per-voxel 1/(mua V N) factor once and applies it to all gates;
-// up to 8 gate loads are in flight before the first store. No integer division.
+// PAIR of consecutive voxels (16-byte int64x2 loads, 8-byte float2 stores);
+// up to 8 gate loads are in flight before the first store. The arithmetic is
+// the reference's, operation for operation, so the f32 volume is bit-identical
+// to FluenceMap::normalize + to_float_volume:
+//   value = (double(cell) * quantum) / den[label],  den = (mua * V) * N
+// (den per label precomputed on the host in the reference's order; den == 0
+// for mua == 0 voxels -> 0); raw mode: value = double(cell) * quantum.
+// Gate-summed (CW) output sums the int64 cells first, like the reference's
+// single map.
+__device__ __forceinline__ float k4_value(long long c, double q, double den, int normalized) {
+  const double raw = static_cast<double>(c) * q;
+  if (!normalized) return static_cast<float>(raw);
+  return den > 0.0 ? static_cast<float>(raw / den) : 0.0f;
+}
+
 __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* __restrict__ labels,
-                            const double* __restrict__ mua, long long nvox, int ngates, int sum_gates,
-                            int normalized, double scale, float* __restrict__ out) {
+                            const double* __restrict__ den, long long nvox, int ngates, int sum_gates,
+                            int normalized, double q, float* __restrict__ out) {
   const long long npair = nvox >> 1;
   const bool vec = (nvox & 1) == 0;  // pairs never straddle a gate boundary
   const long long nwork = vec ? npair : nvox;
@@ -857,13 +878,9 @@ __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* 
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int per = vec ? 2 : 1;
     const long long v0 = i * per;
-    double f[2] = {scale, scale};
-    for (int j = 0; j < per; ++j) {
-      if (normalized) {
-        const double m = mua[__ldg(labels + v0 + j)];
-        f[j] = m > 0.0 ? scale / m : 0.0;
-      }
-    }
+    double d[2] = {0.0, 0.0};
+    if (normalized)
+      for (int j = 0; j < per; ++j) d[j] = den[__ldg(labels + v0 + j)];
     if (sum_gates) {
       long long raw[2] = {0, 0};
       for (int g = 0; g < ngates; ++g) {
@@ -876,10 +893,10 @@ __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* 
         }
       }
       if (vec)
-        __stcs(reinterpret_cast<float2*>(out + v0), make_float2(static_cast<float>(static_cast<double>(raw[0]) * f[0]),
-                                                                static_cast<float>(static_cast<double>(raw[1]) * f[1])));
+        __stcs(reinterpret_cast<float2*>(out + v0),
+               make_float2(k4_value(raw[0], q, d[0], normalized), k4_value(raw[1], q, d[1], normalized)));
       else
-        out[v0] = static_cast<float>(static_cast<double>(raw[0]) * f[0]);
+        out[v0] = k4_value(raw[0], q, d[0], normalized);
     } else {
       for (int g0 = 0; g0 < ngates; g0 += 8) {
         longlong2 buf[8];
@@ -893,9 +910,9 @@ __global__ void k_normalize(const long long* __restrict__ cells, const uint8_t* 
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           if (g0 + k < ngates) {
-            const float a = static_cast<float>(static_cast<double>(buf[k].x) * f[0]);
+            const float a = k4_value(buf[k].x, q, d[0], normalized);
             if (vec) {
-              const float b = static_cast<float>(static_cast<double>(buf[k].y) * f[1]);
+              const float b = k4_value(buf[k].y, q, d[1], normalized);
               __stcs(reinterpret_cast<float2*>(out + v0 + (g0 + k) * nvox), make_float2(a, b));
             } else {
               __stcs(out + v0 + (g0 + k) * nvox, a);
@@ -1247,15 +1264,25 @@ int vmc_plan_normalize(vmc_plan* plan, const int64_t* d_cells, uint64_t photon_c
     ck(cudaSetDevice(plan->device), "cudaSetDevice");
     const long long nvox = static_cast<long long>(plan->nx) * plan->ny * plan->nz;
     const double q = vmc_quantum_for(plan->cfg.photon_count);
+    // den per label in FluenceMap::normalize's order: (mua * v_voxel) * N,
+    // v_voxel = h * h * h (fluence.cpp:66,73-74)
     const double v = plan->voxel_mm * plan->voxel_mm * plan->voxel_mm;
-    const double scale = normalized ? q / (v * static_cast<double>(photon_count)) : q;
+    if (plan->den_n != photon_count) {
+      std::vector<double> mua(static_cast<size_t>(plan->nmedia)), den(mua.size());
+      ck(cudaMemcpy(mua.data(), plan->mua.p, mua.size() * sizeof(double), cudaMemcpyDeviceToHost), "mua");
+      for (size_t m = 0; m < mua.size(); ++m)
+        den[m] = mua[m] > 0.0 ? mua[m] * v * static_cast<double>(photon_count) : 0.0;
+      plan->den.ensure(den.size() * sizeof(double), plan->device);
+      ck(cudaMemcpy(plan->den.p, den.data(), den.size() * sizeof(double), cudaMemcpyHostToDevice), "den");
+      plan->den_n = photon_count;
+    }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
     const long long work = (nvox & 1) ? nvox : nvox / 2;  // voxel pairs when nvox is even
     const int grid = static_cast<int>(std::min<long long>((work + 255) / 256, static_cast<long long>(sms) * 16));
     k_normalize<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const long long*>(d_cells), static_cast<const uint8_t*>(plan->labels.p),
-        static_cast<const double*>(plan->mua.p), nvox, plan->cfg.ngates, sum_gates, normalized, scale, d_out);
+        static_cast<const double*>(plan->den.p), nvox, plan->cfg.ngates, sum_gates, normalized, q, d_out);
     ck(cudaGetLastError(), "launch normalize");
   });
 }

@@ -314,8 +314,13 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       red_cell(q);
     } else if constexpr (kDep == kDepWarp) {
       const unsigned am = __activemask();
-      const int c = cell();
-      const unsigned peers = __match_any_sync(am, c);
+      // the cell's offset in the (gated) map: lanes of different gates never merge
+      unsigned peers;
+      if constexpr (kGates) {
+        peers = __match_any_sync(am, static_cast<unsigned long long>(gmap - cbase) + cell());
+      } else {
+        peers = __match_any_sync(am, cell());
+      }
       if (__all_sync(am, peers == (1u << lane))) {
         red_cell(q);
         return;

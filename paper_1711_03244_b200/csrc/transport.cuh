@@ -125,6 +125,7 @@ struct KernelArgs {
   int pad12;
 };
 
+
 // ---------------------------------------------------------------------------
 // small helpers
 

@@ -320,10 +320,17 @@ def run_pipeline(setup: RunSetup) -> RunResult:
         raise ValidationError(f"energy conservation violated: relative residual {residual}")
     del t
     if setup.output_path:
+        # `output` is the reference's file: the continuous-wave volume (gates
+        # summed in integers first), nx*ny*nz floats + sidecar (volume_io.cpp:
+        # 26-53), readable by the reference's read_volume. Gate-resolved maps go
+        # to a separate `<output>.gates.raw` (+ its own sidecar with "gates").
         g = setup.scene.grid
-        vol = (res.map.cells.astype(np.float64) * res.map.quantum).astype(np.float32)
-        write_volume(vol, g.dims, g.voxel_size, n, setup.config.master_seed, setup.output_path,
-                     normalized=False, gates=setup.config.ngates)
+        write_volume(res.map.to_float_volume(), g.dims, g.voxel_size, n, setup.config.master_seed,
+                     setup.output_path, normalized=False)
+        if setup.config.ngates > 1:
+            vol = (res.map.cells.astype(np.float64) * res.map.quantum).astype(np.float32)
+            write_volume(vol, g.dims, g.voxel_size, n, setup.config.master_seed, setup.output_path + ".gates.raw",
+                         normalized=False, gates=setup.config.ngates)
     if setup.report_path:
         with open(setup.report_path, "w") as f:
             f.write(report_to_json(rep) + "\n")

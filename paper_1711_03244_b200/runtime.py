@@ -128,7 +128,7 @@ class FluenceMap:
 
     def value(self, cell: int) -> float:
         if self._values is not None:
-            return float(self._values.reshape(-1)[cell])
+            return float(self._cw_values.reshape(-1)[cell])
         return float(self.cw_cells()[cell]) * self.quantum
 
     def total_deposited(self) -> float:
@@ -148,17 +148,22 @@ class FluenceMap:
             raise AlreadyNormalized("FluenceMap::normalize: already normalized")
         if grid.dims != self.dims:
             raise DimensionMismatch("FluenceMap::normalize: grid dims differ")
+        # the reference's order: (double(cell) * quantum) / ((mua * v) * N),
+        # v = h * h * h; gate-resolved values per gate, and the CW values from
+        # the gate-summed cells (the reference's single map)
         mua = grid.media_array()[:, 0][grid.labels.astype(np.int64)].reshape(self.dims[::-1])
-        v = grid.voxel_size ** 3
-        raw = self.cells.astype(np.float64) * self.quantum
+        h = float(grid.voxel_size)
+        den = mua * (h * h * h) * float(self.photon_count)
         with np.errstate(divide="ignore", invalid="ignore"):
-            vals = np.where(mua > 0.0, raw / (mua * v * float(self.photon_count)), 0.0)
+            vals = np.where(mua > 0.0, (self.cells.astype(np.float64) * self.quantum) / den, 0.0)
+            cw = np.where(mua > 0.0, (self.cells.sum(axis=0).astype(np.float64) * self.quantum) / den, 0.0)
         self.zero_mua_voxels = int((mua <= 0.0).sum())
         self._values = vals
+        self._cw_values = cw
 
     def to_float_volume(self) -> np.ndarray:  # fluence.cpp:86-90 (CW, x fastest)
         if self._values is not None:
-            return self._values.sum(axis=0).astype(np.float32).reshape(-1)
+            return self._cw_values.astype(np.float32).reshape(-1)
         return (self.cw_cells().astype(np.float64) * self.quantum).astype(np.float32)
 
 

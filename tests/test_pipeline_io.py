@@ -109,7 +109,7 @@ def test_run_pipeline_and_normalize(gpu, tmp_path):
     plan.normalize_torch(cells, phi, 200_000)
     r.map.normalize(st.grid)
     host = r.map.to_float_volume()
-    assert np.allclose(phi.cpu().numpy(), host, rtol=1e-6, atol=0)
+    assert np.array_equal(phi.cpu().numpy(), host)  # same arithmetic, bit for bit
 
 
 @pytest.mark.gpu
@@ -134,6 +134,83 @@ def test_normalize_kernel_odd_even_gates(gpu, dims, ngates):
     torch.cuda.synchronize()
     fm = v.FluenceMap(dims, 12345, ngates, cells)
     fm.normalize(grid)
-    assert np.allclose(per.cpu().numpy(), fm._values.reshape(-1).astype(np.float32), rtol=1e-6)
-    assert np.allclose(cw.cpu().numpy(), fm._values.sum(axis=0).reshape(-1).astype(np.float32), rtol=1e-5)
+    assert np.array_equal(per.cpu().numpy(), fm._values.reshape(-1).astype(np.float32))
+    assert np.array_equal(cw.cpu().numpy(), fm.to_float_volume())
     assert np.all(per.cpu().numpy().reshape(ngates, -1)[:, lab == 2] == 0)  # mua == 0 -> 0
+
+
+def _random_map(rng, dims, ngates, photons):
+    nx, ny, nz = dims
+    lab = rng.integers(0, 3, nx * ny * nz).astype(np.uint8)
+    media = [v.OpticalProperties(), v.OpticalProperties(0.02, 1.0, 0.5, 1.3),
+             v.OpticalProperties(0.0173, 1.0, 0.5, 1.3)]
+    grid = v.VoxelGrid(dims, 0.7, lab, media)
+    scene = v.Scene(grid, v.Source((1.0, 1.0, 0.0), (0.0, 0.0, 1.0)))
+    # magnitudes past 2^53 included (double(cell) rounds, as in the reference)
+    cells = rng.integers(0, 1 << 60, ngates * grid.voxel_count).astype(np.int64) >> rng.integers(
+        0, 40, ngates * grid.voxel_count)
+    return scene, cells
+
+
+@pytest.mark.parametrize("normalized", [True, False])
+def test_host_normalize_equals_reference(ref, normalized):
+    """FluenceMap.normalize / to_float_volume (runtime.py) against the compiled
+    reference's FluenceMap::normalize + to_float_volume (fluence.cpp:62-90), bit
+    for bit, for the CW map and for every gate of a gated map."""
+    rng = np.random.default_rng(11)
+    scene, cells = _random_map(rng, (7, 5, 6), 3, 987_654)
+    fm = v.FluenceMap(scene.grid.dims, 987_654, 3, cells)
+    if normalized:
+        fm.normalize(scene.grid)
+    want_cw = ref.normalize(scene, 987_654, fm.cells.sum(axis=0), normalized)
+    assert np.array_equal(fm.to_float_volume(), want_cw)
+    if normalized:
+        for g in range(3):
+            want = ref.normalize(scene, 987_654, fm.cells[g], True)
+            assert np.array_equal(fm._values[g].reshape(-1).astype(np.float32), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,ngates", [((7, 5, 6), 3), ((8, 4, 6), 10), ((60, 60, 60), 1)])
+def test_normalize_kernel_equals_reference(gpu, ref, dims, ngates):
+    """K4 (vmc_plan_normalize) against the compiled reference's
+    FluenceMap::normalize + to_float_volume (fluence.cpp:62-90): bit for bit,
+    per gate, gate-summed, and raw (unnormalized) export."""
+    import torch
+    rng = np.random.default_rng(5)
+    scene, cells = _random_map(rng, dims, ngates, 123_457)
+    cfg = v.SimulationConfig(photon_count=123_457, ngates=ngates)
+    plan = gpu.Plan(scene, cfg)
+    tc = torch.from_numpy(cells).cuda()
+    nvox = scene.grid.voxel_count
+    for normalized in (True, False):
+        per = torch.zeros(plan.ncells, dtype=torch.float32, device="cuda")
+        cw = torch.zeros(nvox, dtype=torch.float32, device="cuda")
+        plan.normalize_torch(tc, per, 123_457, sum_gates=False, normalized=normalized)
+        plan.normalize_torch(tc, cw, 123_457, sum_gates=True, normalized=normalized)
+        torch.cuda.synchronize()
+        per_h = per.cpu().numpy().reshape(ngates, -1)
+        c = cells.reshape(ngates, -1)
+        for g in range(ngates):
+            assert np.array_equal(per_h[g], ref.normalize(scene, 123_457, c[g], normalized)), (g, normalized)
+        assert np.array_equal(cw.cpu().numpy(), ref.normalize(scene, 123_457, c.sum(axis=0), normalized))
+    plan.close()
+
+
+@pytest.mark.gpu
+def test_gated_pipeline_output_keeps_reference_format(gpu, tmp_path):
+    """With time gates, `output` stays the reference's nx*ny*nz float file (the
+    gate-summed volume, read_volume-compatible: volume_io.cpp:60-88) and the
+    gate-resolved volume goes to `<output>.gates.raw`."""
+    st = v.baseline_setup("b1", photons=50_000)
+    st.config.ngates = 5
+    out = str(tmp_path / "g.raw")
+    r = P.run_pipeline(P.RunSetup(st.scene, st.config, output_path=out))
+    vol = read_volume(out)
+    assert vol.gates == 1 and vol.values.size == st.grid.voxel_count
+    assert os.path.getsize(out) == 4 * st.grid.voxel_count
+    assert np.array_equal(vol.values, r.map.to_float_volume())
+    assert "gates" not in json.load(open(out + ".json"))
+    gv = read_volume(out + ".gates.raw")
+    assert gv.gates == 5 and gv.values.size == 5 * st.grid.voxel_count
+    assert np.array_equal(gv.values, (r.map.cells.astype(np.float64) * r.map.quantum).astype(np.float32).reshape(-1))

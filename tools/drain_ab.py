@@ -1,0 +1,35 @@
+"""A/B of the drain loop threshold (VMC_DRAIN_LANES; 0 = no drain loop):
+device photons/ms of one run_group_dynamic call, best of 3, per photon count.
+usage: python tools/drain_ab.py [workloads] [thresholds]"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r"""
+import sys, json
+sys.path.insert(0, %r)
+import paper_1711_03244_b200 as v
+out = {}
+for name in %r:
+    for n in (100_000, 1_000_000, 10_000_000, 100_000_000):
+        st = v.baseline_setup(name, photons=n)
+        best = min(v.run_group_dynamic(0, n, 1, st.scene, st.config).wall_ms for _ in range(3))
+        out[f"{name}@{n:.0e}"] = n / best
+print(json.dumps(out))
+"""
+
+if __name__ == "__main__":
+    work = sys.argv[1].split(",") if len(sys.argv) > 1 else ["b1", "b2"]
+    thr = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 4, 8, 16, 32]
+    res = {}
+    for t in thr:
+        env = dict(os.environ, VMC_DRAIN_LANES=str(t))
+        r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, work)], env=env, capture_output=True, text=True)
+        if r.returncode:
+            print(r.stderr[-2000:], file=sys.stderr)
+            continue
+        res[t] = json.loads(r.stdout.strip().splitlines()[-1])
+        print(t, {k: round(x) for k, x in res[t].items()}, flush=True)
+    print(json.dumps(res))
