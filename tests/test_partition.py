@@ -82,3 +82,37 @@ def test_simulated_calibration():
     flat = v.DeviceProfile(name="weird", a=0.0, t0=100.0, kind=v.DeviceKind.Simulated)
     with pytest.raises(v.NonPositiveSlope):
         v.calibrate(flat, 1000, 2000, st.scene, st.config)
+
+
+def test_live_reference_ties_and_identical_devices(ref):
+    """Identical and commensurate devices make many optimal S3 allocations tie;
+    the split must still be the reference's, device for device (which device
+    gets a tied unit depends on the FMA-rounded finish times a*n + t0)."""
+    rnd = random.Random(9)
+    cases = []
+    for k in (1, 2, 3, 4, 8, 16, 17):
+        for total in (0, 1, 2, 5, 7, 1000, 10**9 + 7):
+            cases += [([(1, 1e-6, 0.1)] * k, total), ([(1, 1e-6, 0.0)] * k, total),
+                      ([(1, 2e-6, 0.0), (1, 1e-6, 0.0)] * (k // 2 or 1), total),
+                      ([(1, 1e-3, 5.0), (2, 1e-3, 0.0), (1, 1e-3, 5.0)] * (k // 3 or 1), total)]
+    for _ in range(300):
+        k = rnd.randint(1, 16)
+        ps = [(rnd.randint(1, 64), rnd.choice([1e-6, 2e-6, 0.5, 0.25, rnd.uniform(1e-7, 1e-3)]),
+               rnd.choice([0.0, 0.1, 1.0, rnd.uniform(0, 50)])) for _ in range(k)]
+        cases.append((ps, rnd.choice([rnd.randint(0, 10**9), rnd.randint(0, 100)])))
+    for ps, total in cases:
+        for s in (1, 2, 3):
+            want, _ = ref.partition(s, total, ps)
+            if sum(want) != total:
+                continue  # the reference's numerical corner, see the next test
+            assert v.make_partition(total, profs(ps), v.Strategy(s)).counts == want, (s, total, ps)
+
+
+def test_s3_covers_total_where_the_reference_returns_zeros(ref):
+    """One device, 1e9 photons: the reference's bisection capacities
+    floor((T - t0)/a + 1e-9) fall one photon short at its upper bound, so its
+    S3 returns an all-zero split (scheduler.cpp:126-131,160). The B200 split
+    gives the device every photon (the only valid split)."""
+    want, _ = ref.partition(3, 10**9, [(1, 1e-6, 0.1)])
+    assert want == [0]
+    assert v.partition_s3(10**9, profs([(1, 1e-6, 0.1)])).counts == [10**9]
