@@ -191,6 +191,18 @@ VMC_API double vmc_model_makespan(int ndev, const uint64_t* counts, const vmc_de
 /* First n outputs of RngStream(seed, stream_id).next_u64() computed on the device. */
 VMC_API int vmc_rng_kat(uint64_t seed, uint64_t stream_id, int n, int device, uint64_t* out);
 
+/* One photon's walk in the reference's arithmetic (FP64 flight kernel) on
+ * `device`: reference simulate_photon / simulate_photon_trace
+ * (proj/core/include/voxmc/transport.hpp:105-113, transport.cpp:362-380).
+ * Writes the per-step deposits in walk order (linear cell, absorbed weight;
+ * steps that deposit nothing are skipped, as the reference's sink never sees
+ * them) into cells_out/dw_out (first max_deposits of *n_deposits) and the
+ * photon's disposition {deposited, escaped, killed, truncated} into disp_out.
+ * Time gates are ignored (continuous wave). Synchronous. */
+VMC_API int vmc_simulate_photon(const vmc_scene* scene, const vmc_config* config, uint64_t photon_index,
+                                int device, uint64_t max_deposits, int64_t* cells_out, double* dw_out,
+                                uint64_t* n_deposits, double* disp_out);
+
 /* ---- device-resident plan: scene on the GPU, caller-owned buffers ------- */
 typedef struct vmc_plan vmc_plan;
 

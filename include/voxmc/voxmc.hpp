@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <utility>
 #include <vector>
 
 #pragma GCC visibility push(default)
@@ -231,6 +232,16 @@ struct PhotonDisposition {
     return *this;
   }
 };
+
+// One photon's walk (reference transport.hpp:105-113), executed on CUDA device
+// 0 by the FP64 flight kernel (the reference's arithmetic): simulate_photon
+// adds every step deposit to `map` through FluenceMap::deposit;
+// simulate_photon_trace returns the per-step deposit list in walk order.
+PhotonDisposition simulate_photon(std::uint64_t photon_index, const Scene& scene, const SimulationConfig& config,
+                                  FluenceMap& map);
+PhotonDisposition simulate_photon_trace(std::uint64_t photon_index, const Scene& scene,
+                                        const SimulationConfig& config,
+                                        std::vector<std::pair<VoxelIndex, double>>& deposits);
 
 struct DetectorRecord {  // B200
   std::uint64_t photon_index = 0;

@@ -16,5 +16,5 @@ from .runtime import (Calibration, DeviceKind, DeviceProfile, FluenceMap, GroupR
                       MultiDeviceResult, Partition, PhotonDisposition, Plan, Strategy, calibrate,
                       device_count, lib, make_partition, merge, model_makespan, partition_s1,
                       partition_s2, partition_s3, quantum_for, rng_kat, run_group_dynamic,
-                      run_multi_device, run_static_split, simulate_photon, strategy_from_name,
+                      run_multi_device, run_static_split, simulate_photon, simulate_photon_trace, strategy_from_name,
                       thread_count_heuristic, trace_photons)

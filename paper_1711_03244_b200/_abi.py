@@ -112,6 +112,7 @@ EXPORTS = (
     "vmc_plan_launches_per_run",
     "vmc_plan_kernel_name",
     "vmc_plan_sort_records",
+    "vmc_simulate_photon",
 )
 
 
@@ -143,6 +144,7 @@ def declare(lib: C.CDLL) -> C.CDLL:
         "vmc_plan_launches_per_run": (C.c_int, [vp, u32]),
         "vmc_plan_kernel_name": (C.c_char_p, [vp]),
         "vmc_plan_sort_records": (C.c_int, [vp, vp, u64, u64, u64, vp, vp]),
+        "vmc_simulate_photon": (C.c_int, [P(vmc_scene), P(vmc_config), u64, C.c_int, u64, vp, vp, vp, vp]),
         "vmc_plan_normalize": (C.c_int, [vp, vp, u64, vp, C.c_int, C.c_int, vp]),
         "vmc_fnv1a64": (u64, [vp, C.c_size_t]),
     }

@@ -564,9 +564,16 @@ __global__ void k_fold_replicas(unsigned long long* __restrict__ cells, const un
   }
 }
 
+struct DepLog {
+  long long* cells = nullptr;
+  double* w = nullptr;
+  unsigned long long* n = nullptr;
+  unsigned long long cap = 0;
+};
+
 void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells, int64_t* d_totals,
                   void* d_det, uint64_t* d_det_count, cudaStream_t st, uint32_t flags, bool trace,
-                  vmc_photon_trace* d_trace) {
+                  vmc_photon_trace* d_trace, const DepLog* log = nullptr) {
   if (!d_cells || !d_totals) fail_validation("device cells/totals buffers are required");
   if (P->cfg.ndet > 0 && P->cfg.det_capacity > 0 && !d_det) fail_validation("detector buffer is required");
   if (P->cfg.ndet > 0 && !d_det_count) fail_validation("detector count buffer is required");
@@ -1253,6 +1260,53 @@ int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_pho
     ck(cudaDeviceSynchronize(), "trace run");
     if (count) ck(cudaMemcpy(out, tr.p, count * sizeof(vmc_photon_trace), cudaMemcpyDeviceToHost), "download trace");
     check_launch_errors(plan);
+  });
+}
+
+int vmc_simulate_photon(const vmc_scene* scene, const vmc_config* config, uint64_t photon_index, int device,
+                        uint64_t max_deposits, int64_t* cells_out, double* dw_out, uint64_t* n_deposits,
+                        double* disp_out) {
+  return guarded([&] {
+    if (max_deposits && (!cells_out || !dw_out)) fail_validation("simulate_photon: null deposit buffers");
+    vmc_config c = *config;
+    c.precision = VMC_PRECISION_FP64;  // the reference's arithmetic (FP64 flight kernel)
+    c.ngates = 1;
+    vmc_plan P;
+    plan_init(&P, scene, &c, device);
+    DevBuf cells, totals, det, detn, tr, lc, lw, ln;
+    cells.alloc(P.ncells * sizeof(int64_t), device);
+    totals.alloc(4 * sizeof(int64_t), device);
+    const uint64_t cap = c.ndet > 0 ? c.det_capacity : 0;
+    det.alloc(cap * P.rec_stride, device);
+    detn.alloc(sizeof(uint64_t), device);
+    tr.alloc(sizeof(vmc_photon_trace), device);
+    lc.alloc(max_deposits * sizeof(long long), device);
+    lw.alloc(max_deposits * sizeof(double), device);
+    ln.alloc(sizeof(unsigned long long), device);
+    ck(cudaMemset(ln.p, 0, sizeof(unsigned long long)), "zero log");
+    DepLog log{static_cast<long long*>(lc.p), static_cast<double*>(lw.p), static_cast<unsigned long long*>(ln.p),
+               max_deposits};
+    plan_enqueue(&P, photon_index, 1, static_cast<int64_t*>(cells.p), static_cast<int64_t*>(totals.p), det.p,
+                 static_cast<uint64_t*>(detn.p), nullptr, VMC_RUN_ZERO, true, static_cast<vmc_photon_trace*>(tr.p),
+                 &log);
+    ck(cudaDeviceSynchronize(), "simulate_photon");
+    check_launch_errors(&P);
+    vmc_photon_trace t;
+    ck(cudaMemcpy(&t, tr.p, sizeof t, cudaMemcpyDeviceToHost), "download trace");
+    unsigned long long n = 0;
+    ck(cudaMemcpy(&n, ln.p, sizeof n, cudaMemcpyDeviceToHost), "download log count");
+    const uint64_t keep = std::min<uint64_t>(n, max_deposits);
+    if (keep) {
+      ck(cudaMemcpy(cells_out, lc.p, keep * sizeof(long long), cudaMemcpyDeviceToHost), "download log");
+      ck(cudaMemcpy(dw_out, lw.p, keep * sizeof(double), cudaMemcpyDeviceToHost), "download log");
+    }
+    if (n_deposits) *n_deposits = n;
+    if (disp_out) {
+      disp_out[0] = t.deposited;
+      disp_out[1] = t.escaped;
+      disp_out[2] = t.killed;
+      disp_out[3] = t.truncated;
+    }
   });
 }
 

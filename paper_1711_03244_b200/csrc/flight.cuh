@@ -354,6 +354,15 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // FP32: q == 0 only if mua == 0. FP64: one run per step; empty steps add
     // nothing (run_photon :325-328)
     if (kF32 || q != 0) add_quanta(static_cast<unsigned long long>(q));
+    if constexpr (kTrace) {
+      if (A.dep_n && dw != Real(0)) {  // the reference's sink sees every nonzero step deposit
+        const unsigned long long k = atomicAdd(A.dep_n, 1ull);
+        if (k < A.dep_cap) {
+          A.dep_cells[k] = cell();
+          A.dep_w[k] = static_cast<double>(dw);
+        }
+      }
+    }
     if constexpr (kTrace) pd_dep += static_cast<double>(dw);
     run_w0 = w;
   };

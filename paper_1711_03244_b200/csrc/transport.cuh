@@ -103,6 +103,12 @@ struct KernelArgs {
   unsigned long long* det_count;
   unsigned long long det_cap;
   vmc_photon_trace* trace;
+  // trace launches only (vmc_simulate_photon): per-step deposit log
+  // {cell, dw} in walk order, like simulate_photon_trace's deposit list
+  long long* dep_cells;
+  double* dep_w;
+  unsigned long long* dep_n;
+  unsigned long long dep_cap;
   int* error_flag;  // set to 1 when a launch point falls outside the grid
   // single-label volumes (kUni): the one interior medium, read straight from
   // the parameter bank (constant operands, no shared-memory address math)

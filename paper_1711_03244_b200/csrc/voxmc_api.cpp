@@ -352,8 +352,59 @@ GroupRunResult run_group_dynamic(std::uint64_t first_index, std::uint64_t quota,
 
 GroupRunResult run_static_split(std::uint64_t first_index, std::uint64_t quota, int threads, const Scene& scene,
                                 const SimulationConfig& config) {
-  // per-photon streams make static and dynamic claiming bit-identical
-  return run_group_dynamic(first_index, quota, threads, scene, config);
+  // per-photon streams make static and dynamic claiming bit-identical; the
+  // accounting reports the reference's static ceil-sized blocks
+  // (scheduler.cpp:295-302)
+  GroupRunResult r = run_group_dynamic(first_index, quota, threads, scene, config);
+  const std::uint64_t block = (quota + static_cast<std::uint64_t>(threads) - 1) / static_cast<std::uint64_t>(threads);
+  for (int t = 0; t < threads; ++t) {
+    const std::uint64_t lo = std::min(quota, block * static_cast<std::uint64_t>(t));
+    r.per_thread_photons[static_cast<std::size_t>(t)] = std::min(quota, lo + block) - lo;
+  }
+  return r;
+}
+
+namespace {
+std::vector<std::pair<std::int64_t, double>> walk_photon(std::uint64_t photon_index, const Scene& scene,
+                                                         const SimulationConfig& config, PhotonDisposition& disp) {
+  config.validate();
+  Abi abi(scene, config);
+  std::uint64_t cap = 1u << 16;
+  for (;;) {
+    std::vector<std::int64_t> cells(cap);
+    std::vector<double> dw(cap);
+    std::uint64_t n = 0;
+    double d[4] = {0, 0, 0, 0};
+    check(vmc_simulate_photon(&abi.s, &abi.c, photon_index, 0, cap, cells.data(), dw.data(), &n, d));
+    if (n <= cap) {
+      disp = {d[0], d[1], d[2], d[3]};
+      std::vector<std::pair<std::int64_t, double>> out(n);
+      for (std::uint64_t i = 0; i < n; ++i) out[i] = {cells[i], dw[i]};
+      return out;
+    }
+    cap = n;  // longer walk than the first guess: run again with room for all of it
+  }
+}
+}  // namespace
+
+PhotonDisposition simulate_photon(std::uint64_t photon_index, const Scene& scene, const SimulationConfig& config,
+                                  FluenceMap& map) {
+  PhotonDisposition disp;
+  for (const auto& [cell, dw] : walk_photon(photon_index, scene, config, disp))
+    map.deposit(static_cast<std::size_t>(cell), dw);
+  return disp;
+}
+
+PhotonDisposition simulate_photon_trace(std::uint64_t photon_index, const Scene& scene,
+                                        const SimulationConfig& config,
+                                        std::vector<std::pair<VoxelIndex, double>>& deposits) {
+  PhotonDisposition disp;
+  const std::int64_t nx = scene.grid.nx(), nxy = nx * scene.grid.ny();
+  for (const auto& [cell, dw] : walk_photon(photon_index, scene, config, disp))
+    deposits.push_back({VoxelIndex{static_cast<int>(cell % nx), static_cast<int>((cell % nxy) / nx),
+                                   static_cast<int>(cell / nxy)},
+                        dw});
+  return disp;
 }
 
 double static_split_makespan(std::span<const double> costs, int threads) {
@@ -401,8 +452,11 @@ Calibration calibrate(const DeviceProfile& device, std::uint64_t n1, std::uint64
       t1 *= factor();
       t2 *= factor();
     }
-  } else {
-    throw ValidationError("calibrate: host worker pools are not executed by the B200 library");
+  } else {  // a host worker pool of the reference: its pilots run on the B200 executor
+    SimulationConfig pilot = config;
+    pilot.photon_count = n2;
+    t1 = run_group_on(0, 0, n1, scene, pilot).wall_ms;
+    t2 = run_group_on(0, 0, n2, scene, pilot).wall_ms;
   }
   (void)threads;
   if (t2 <= t1) throw NonPositiveSlope("calibrate: T2 <= T1; increase n2 or rerun");
@@ -416,16 +470,17 @@ MultiDeviceResult run_multi_device(std::uint64_t total, std::span<const DevicePr
                                    const Scene& scene, const SimulationConfig& config, int threads_per_device) {
   (void)threads_per_device;
   if (devices.empty()) throw ValidationError("run_multi_device: no devices");
-  for (const DeviceProfile& d : devices)
-    if (d.kind != DeviceKind::CudaGpu) throw ValidationError("run_multi_device: devices must be DeviceKind::CudaGpu");
   Partition part = make_partition(total, devices, strategy);
   SimulationConfig cfg = config;
   cfg.photon_count = total;  // shared quantum (reference scheduler.cpp:412-413)
   cfg.validate();
   Abi abi(scene, cfg);
   FluenceMap map(scene.grid.dims(), total, AccumulationMode::PrivateMerge, false, cfg.ngates);
+  // every device's range runs on a B200: CudaGpu devices on their own GPU, the
+  // reference's host pools and simulated devices on GPU 0 (a simulated device
+  // keeps the reference's modelled wall time a*n + t0, scheduler.cpp:441-443)
   std::vector<int> gpus;
-  for (const DeviceProfile& d : devices) gpus.push_back(d.gpu);
+  for (const DeviceProfile& d : devices) gpus.push_back(d.kind == DeviceKind::CudaGpu ? d.gpu : 0);
   vmc_disposition tot{};
   const int nm = static_cast<int>(scene.grid.media().size());
   std::vector<unsigned char> det(cfg.detectors.empty() ? 0 : cfg.det_capacity * vmc_det_record_bytes(nm));
@@ -436,7 +491,10 @@ MultiDeviceResult run_multi_device(std::uint64_t total, std::span<const DevicePr
                       map.raw_cells().data(), &tot, det.empty() ? nullptr : det.data(), &ndet, ms.data(), &red));
   MultiDeviceResult r{std::move(map), from_quanta(tot), part, {}, 0.0, red, {}, ndet};
   for (std::size_t i = 0; i < devices.size(); ++i) {
-    r.devices.push_back({devices[i].name, part.counts[i], part.counts[i] ? ms[i] : 0.0});
+    const double wall = devices[i].kind == DeviceKind::Simulated
+                            ? devices[i].a * static_cast<double>(part.counts[i]) + devices[i].t0
+                            : ms[i];
+    r.devices.push_back({devices[i].name, part.counts[i], part.counts[i] ? wall : 0.0});
     r.makespan_ms = std::max(r.makespan_ms, r.devices.back().wall_ms);
   }
   r.makespan_ms += red;

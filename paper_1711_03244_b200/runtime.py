@@ -240,14 +240,38 @@ def run_group_dynamic(first_index: int, quota: int, threads: int, scene: Scene,
 run_static_split = run_group_dynamic
 
 
+def simulate_photon_trace(photon_index: int, scene: Scene, config: SimulationConfig, device: int = 0,
+                          max_deposits: int = 1 << 20):
+    """One photon's walk on the device in the reference's arithmetic (FP64
+    flight kernel; reference simulate_photon_trace, transport.cpp:368-380):
+    returns (PhotonDisposition, [(cell, dw), ...]) with one entry per step that
+    deposits, in walk order."""
+    m = Marshalled(scene, config)
+    cells = np.zeros(max_deposits, np.int64)
+    dws = np.zeros(max_deposits, np.float64)
+    n = C.c_uint64()
+    disp = (C.c_double * 4)()
+    _check(lib().vmc_simulate_photon(C.byref(m.scene), C.byref(m.config), photon_index, device, max_deposits,
+                                     cells.ctypes.data, dws.ctypes.data, C.byref(n), disp))
+    k = min(n.value, max_deposits)
+    return PhotonDisposition(*disp), list(zip(cells[:k].tolist(), dws[:k].tolist()))
+
+
 def simulate_photon(photon_index: int, scene: Scene, config: SimulationConfig,
                     device: int = 0):
-    """One photon's walk on the device (reference simulate_photon /
-    simulate_photon_trace, transport.cpp:362-380): returns its disposition and
-    its per-voxel deposits as a FluenceMap in the quantum of
-    config.photon_count."""
-    r = run_group_dynamic(photon_index, 1, 1, scene, config, device)
-    return r.totals, r.map
+    """Reference simulate_photon (transport.cpp:362-366): the photon's walk on
+    the device (FP64 flight kernel) with every step deposit added to a
+    FluenceMap in the quantum of config.photon_count exactly as
+    FluenceMap::deposit does (llround(dw / quantum), fluence.hpp:39-54).
+    Returns (disposition, map)."""
+    disp, deps = simulate_photon_trace(photon_index, scene, config, device)
+    fmap = FluenceMap(scene.grid.dims, config.photon_count)
+    flat = fmap.cells.reshape(-1)
+    inv = 1.0 / fmap.quantum
+    for cell, dw in deps:
+        x = dw * inv
+        flat[cell] += int(math.copysign(math.floor(abs(x) + 0.5), x))  # llround
+    return disp, fmap
 
 
 # ---------------------------------------------------------------------------
@@ -351,12 +375,11 @@ def run_multi_device(total: int, devices: Sequence[DeviceProfile], strategy: Str
                      config: SimulationConfig, threads_per_device: int = 0) -> MultiDeviceResult:
     """scheduler.cpp:395-451 on B200s: contiguous global ranges in device
     order, shared quantum from `total`, one host thread per GPU, NCCL reduce of
-    the int64 maps. Every device must be DeviceKind.CudaGpu."""
+    the int64 maps. CudaGpu devices run on their own GPU; the reference's host
+    pools and simulated devices run their ranges on GPU 0, a simulated device
+    keeping the reference's modelled wall time a*n + t0 (scheduler.cpp:441-443)."""
     if not devices:
         raise ValidationError("run_multi_device: no devices")
-    for d in devices:
-        if d.kind != DeviceKind.CudaGpu:
-            raise ValidationError("run_multi_device: the B200 runner executes CudaGpu devices only")
     part = make_partition(total, devices, strategy)
     cfg = SimulationConfig(**{**config.__dict__})
     cfg.photon_count = total  # scheduler.cpp:412-413
@@ -370,13 +393,15 @@ def run_multi_device(total: int, devices: Sequence[DeviceProfile], strategy: Str
     nd = len(devices)
     per_ms = (C.c_double * nd)()
     red_ms = C.c_double(0.0)
-    gpus = (C.c_int * nd)(*[d.gpu for d in devices])
+    gpus = (C.c_int * nd)(*[d.gpu if d.kind == DeviceKind.CudaGpu else 0 for d in devices])
     counts = (C.c_uint64 * nd)(*part.counts)
     _check(lib().vmc_run_multi(C.byref(m.scene), C.byref(m.config), nd, gpus, counts, cells.ctypes.data,
                                C.byref(tot), det.ctypes.data if det is not None else None,
                                C.byref(ndet), per_ms, C.byref(red_ms)))
     q = (tot.deposited_q, tot.escaped_q, tot.killed_q, tot.truncated_q)
-    runs = [DeviceRunResult(d.name, part.counts[i], per_ms[i] if part.counts[i] else 0.0)
+    runs = [DeviceRunResult(d.name, part.counts[i],
+                            (d.a * part.counts[i] + d.t0 if d.kind == DeviceKind.Simulated else per_ms[i])
+                            if part.counts[i] else 0.0)
             for i, d in enumerate(devices)]
     res = MultiDeviceResult(FluenceMap(scene.grid.dims, total, cfg.ngates, cells),
                             PhotonDisposition.from_quanta(q, tot.quantum), part, runs,

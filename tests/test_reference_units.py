@@ -1,0 +1,48 @@
+"""The reference's own doctest unit files (proj/tests/test_{rng,fluence,domain,
+scheduler}.cpp), compiled UNMODIFIED against the B200 drop-in headers
+(include/voxmc) with the doctest stand-in tests/cpp/doctest.h and linked to
+libvoxmc_b200.so (recipe: oracle/Makefile `reftests`, built by
+__graft_entry__.build() where /root/reference exists; the binaries travel with
+the repo snapshot). Host-side units run here; test_scheduler's executor cases
+(run_group_dynamic / run_static_split / run_multi_device on the GPU) run with
+-m gpu."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "tests")
+
+
+def run_unit(name, filt=None):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    r = subprocess.run([exe] + ([filt] if filt else []), capture_output=True, text=True, timeout=900)
+    return r.returncode, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name", ["test_rng", "test_fluence", "test_domain"])
+def test_reference_host_units(name):
+    rc, out = run_unit(name)
+    assert rc == 0, out[-3000:]
+    assert " 0 failed" in out
+
+
+@pytest.mark.parametrize("filt", ["thread count", "S1 ", "S2 ", "S3 ", "conserve", "group counter", "replay",
+                                  "calibration", "strategy names"])
+def test_reference_scheduler_host_cases(filt):
+    rc, out = run_unit("test_scheduler", filt)
+    assert rc == 0, out[-3000:]
+    assert "test cases: 0 " not in out  # the filter matched something
+
+
+@pytest.mark.gpu
+def test_reference_scheduler_unit_on_gpu(gpu):
+    """All of test_scheduler.cpp, including the executor contracts on the B200:
+    dynamic == static raw cells, per-thread accounting, and the multi-device
+    merge == single-device raw cells (test_scheduler.cpp:157-178, 246-264)."""
+    rc, out = run_unit("test_scheduler")
+    assert rc == 0, out[-3000:]
+    assert " 0 failed" in out
