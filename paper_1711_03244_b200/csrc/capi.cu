@@ -603,6 +603,12 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   A.det_out = static_cast<unsigned char*>(d_det);
   A.det_count = reinterpret_cast<unsigned long long*>(d_det_count);
   A.trace = d_trace;
+  if (trace && log) {  // vmc_simulate_photon: per-step deposit log
+    A.dep_cells = log->cells;
+    A.dep_w = log->w;
+    A.dep_n = log->n;
+    A.dep_cap = log->cap;
+  }
   // never launch more persistent threads than photons need
   const uint64_t need_blocks = (count + P->block - 1) / P->block;
   const int full = trace ? P->grid_trace : P->grid;
