@@ -250,8 +250,8 @@ VMC_API int vmc_plan_sort_records(vmc_plan* plan, const void* d_recs, uint64_t n
                                   uint64_t count, void* d_out, void* stream);
 
 /* Mangled device symbol of the transport kernel variant this plan launches
- * (e.g. _ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi1ELi0EEEvNS_10KernelArgsE = the FP32
- * gated multi-label Taylor-5 K1f); "" when unavailable. Valid while the plan lives. */
+ * (e.g. _ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi0EEEvNS_10KernelArgsE = the FP32
+ * gated multi-label K1f with direct deposits); "" when unavailable. Valid while the plan lives. */
 VMC_API const char* vmc_plan_kernel_name(const vmc_plan* plan);
 
 /* Number of kernels vmc_plan_run enqueues per call (for launch accounting). */

@@ -33,7 +33,7 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode, int dep);
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep);
 const void* flight_kernel_double(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
@@ -193,6 +193,7 @@ std::vector<vmc::Medium<Real>> build_media(const vmc_scene* s) {
     M.n = static_cast<Real>(n);
     M.g = static_cast<Real>(g);
     M.iso = std::fabs(g) < 1e-6 ? 1 : 0;  // hg_cos_theta, transport.cpp:121
+    M.ka = static_cast<Real>(-mua * 1.4426950408889634);
     if (!M.iso) {
       M.hg_a = static_cast<Real>((1.0 + g * g) / (2.0 * g));
       M.hg_b = static_cast<Real>(1.0 / (2.0 * g));
@@ -437,12 +438,6 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   // measured: 70-80 flat, 75 best by 0.3 %; clamped so a warp always walks while >= 1 lane of 32 does
   A.event_pct = std::min(100, std::max(4, env_int("VMC_EVENT_PCT", 75)));
   A.walk_keep = (32 * (100 - A.event_pct)) / 100;
-  {
-    double mx = 0.0;
-    for (int m = 0; m < s->nmedia; ++m) mx = std::max(mx, s->media[4 * m]);
-    const double xmax = mx * s->voxel_mm * std::sqrt(3.0);
-    A.absorb_mode = xmax < 0.012 ? 0 : (xmax < 0.15 ? 1 : 2);
-  }
   // K1f (flight.cuh) in the launch's precision unless VMC_KERNEL=step selects
   // the per-step K1 (transport.cuh) for A/B runs. FP64 K1f is the
   // exact-arithmetic pin of the product kernel's structure.
@@ -457,9 +452,6 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     P->kern = vmc::flight_kernel_double(gates, det, false, uniform);
     P->kern_trace = vmc::flight_kernel_double(gates, det, true, uniform);
   } else {
-    // VMC_GENERIC_ABSORB=1 (test hook): the generic variant that picks its
-    // absorb series at run time instead of the compiled-in production one
-    const int abs_sel = env_int("VMC_GENERIC_ABSORB", 0) ? -1 : A.absorb_mode;
     // VMC_DEPOSIT=warp|hotbox: the warp-aggregated / SM-local hot-box deposit
     // paths (A/B; built for the production variants, direct elsewhere)
     const char* dp = std::getenv("VMC_DEPOSIT");
@@ -468,13 +460,13 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     if (dp && std::strcmp(dp, "hotbox") == 0 && s->nx >= vmc::kHotBoxN && s->ny >= vmc::kHotBoxN &&
         s->nz >= vmc::kHotBoxN)
       dep = vmc::kDepHotBox;
-    P->kern = dep != vmc::kDepDirect ? vmc::flight_kernel_float(gates, det, false, uniform, abs_sel, dep) : nullptr;
+    P->kern = dep != vmc::kDepDirect ? vmc::flight_kernel_float(gates, det, false, uniform, dep) : nullptr;
     if (P->kern) {
       P->dep = dep;
     } else {
-      P->kern = vmc::flight_kernel_float(gates, det, false, uniform, abs_sel, vmc::kDepDirect);
+      P->kern = vmc::flight_kernel_float(gates, det, false, uniform, vmc::kDepDirect);
     }
-    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, abs_sel, vmc::kDepDirect);
+    P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, vmc::kDepDirect);
     if (P->dep == vmc::kDepHotBox) {
       // 16^3 box around the source voxel, clamped into the grid
       const int n3[3] = {s->nx, s->ny, s->nz};

@@ -122,12 +122,6 @@ struct FlightOps<double> {
   }
 };
 
-// kAbs: -1 = absorb() picks its series per launch (KernelArgs::absorb_mode);
-// 0 / 1 = compiled for absorb_mode 0 (every mua * h * sqrt(3) < 0.012, the
-// cube60 phantoms) / 1 (< 0.15, the head phantom), which drops the warp-uniform
-// mode tests from every absorb(). The double instantiation always uses the
-// reference's exp_neg.
-//
 // kDep: how a closed deposit run reaches the fluence map (all three give the
 // same integer sums, so bit-identical maps):
 //   kDepDirect  one red.global.add.u64 per run into the CTA's map replica;
@@ -145,7 +139,7 @@ struct FlightOps<double> {
 //               268-275,312-314, at CTA granularity). Ungated kernels only.
 // (kDepDirect / kDepWarp / kDepHotBox, kHotBoxN: transport.cuh)
 
-template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kAbs = -1, int kDep = kDepDirect>
+template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kDep = kDepDirect>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Tr = RealTraits<Real>;
   using F = FlightOps<Real>;
@@ -217,6 +211,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   Real w = 0, tf = 0, rs = 0;  // weight at distance s0 along the flight; time and
                                // remaining scattering length at the flight start
   Real s0 = 0;      // distance along the flight of the last face (or the flight start)
+  Real w_fl = 0;    // FP32: weight at the flight start
   Real run_w0 = 0;  // weight at the start of the open deposit run (one voxel, one gate)
   Real L = 0;       // flight length; sign bit set = the flight ends at the horizon.
                     // FACE: distance of the face event
@@ -233,6 +228,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   unsigned long long* const cbase = reinterpret_cast<unsigned long long*>(A.cells) + roff;
   unsigned long long* gmap = cbase;  // cells of `gate` (gated launches)
   Real fmua = 0, fns = 0;  // current medium (multi-label volumes): mua, n / c
+  Real fka = 0;            // FP32 multi-label volumes: -mua log2(e) of the current medium
   Real sct = 0, sst = 0;  // scatter: cos/sin theta kept across azimuth retries
   uint32_t steps = 0, nscat = 0;
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // trace only
@@ -258,31 +254,22 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       return fns;
     }
   };
-  // Beer-Lambert over the segment [s0, s] of the flight (exp_neg,
-  // transport.cpp:22-27).
-  // FP32: w -= w (1 - exp(-x)) in one rounding, with 1 - exp(-x) from its
-  // Taylor series, so a run's deposit run_w0 - w (exact by Sterbenz) keeps the
-  // step kernel's precision and the weights telescope exactly. The series
-  // order is chosen per launch (warp-uniform branch) from the largest
-  // mua * h * sqrt(3) of the volume: x^3 below 0.012, x^5 below 0.15
-  // (truncation < 1e-7 relative), else x^5 with a MUFU.EX2 fallback.
-  // FP64: w *= exp_neg(x), the reference's degree-4 series below 0.01, else exp.
+  // Beer-Lambert along the flight (exp_neg, transport.cpp:22-27).
+  // FP32: w(s) = w_fl 2^(ka s), ka = -mua log2(e), from the weight at the
+  // flight start in one MUFU.EX2 (3 instructions per face instead of a Taylor
+  // chain on the segment); a run's deposit run_w0 - w is an exact difference
+  // of two stored weights, so the deposits along a flight telescope exactly
+  // (A/B on B200: +1.9 % B1/B2, +3.2 % B3 against the Taylor-3 chain).
+  // FP64: w *= exp_neg(x) per segment, the reference's degree-4 series below
+  // 0.01, else exp.
   auto absorb = [&](Real s) {
-    const Real x = mua_() * (s - s0);
     if constexpr (kF32) {
-      float f;
-      if (kAbs == 0 || (kAbs < 0 && A.absorb_mode == 0)) {
-        f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f)));
-      } else {
-        f = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f - x * (1.0f / 120.0f)))));
-        if (kAbs < 0 && A.absorb_mode == 2 && x >= 0.15f) {
-          float e;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
-          f = 1.0f - e;
-        }
-      }
-      w = fmaf(-w, f, w);
+      float e;
+      const float ka = kUni ? medium(0).ka : fka;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(ka * s));
+      w = w_fl * e;
     } else {
+      const double x = mua_() * (s - s0);
       const double e = x < 0.01 ? 1.0 - x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0)))) : exp(-x);
       w = w * e;
     }
@@ -413,8 +400,10 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if constexpr (!kUni) {
       fmua = M.mua;
       fns = M.ns_per_mm;
+      fka = M.ka;
     }
     s0 = Real(0);
+    w_fl = w;
     const Real ix = Tr::rcp(dx), iy = Tr::rcp(dy), iz = Tr::rcp(dz);  // +-inf for 0
     const int ux = vx, uy = vy, uz = vz;
     const Real t0 = (static_cast<Real>(ux + (dx > Real(0) ? 1 : 0)) * h - px) * ix;

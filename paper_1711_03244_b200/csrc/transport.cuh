@@ -67,7 +67,7 @@ struct alignas(16) Medium {
   Real hg_b, hg_c, hg_d, hg_e;        // hg_b = 1/(2g), hg_c = 1-g^2, hg_d = 1-g, hg_e = 2g
   int nclass;                          // media with equal (double) n share a class
   int iso;                             // |g| < 1e-6
-  int pad0, pad1;
+  Real ka;                             // -mua * log2(e): K1f's exp2-form absorb
 };
 
 struct KernelArgs {
@@ -119,7 +119,7 @@ struct KernelArgs {
   int pad11;
   float gate_wf;  // K1f: gate width tmax / ngates (FP32)
   int event_pct;
-  int absorb_mode;  // K1f absorb(): max mua*h*sqrt(3) < 0.012 -> 0, < 0.15 -> 1, else 2
+  int pad14;
   // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
   // (the host folds the replicas into the caller's map after the launch)
   long long rep_stride;

@@ -60,33 +60,29 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
 
 // K1f (flight.cuh). FP32: the product kernel, same register cap as K1.
 // FP64 (--fmad=false): the exact-arithmetic pin of the same flight structure.
-template <typename R, bool G, bool D, bool T, bool U, int Abs = -1, int Dep = kDepDirect>
+template <typename R, bool G, bool D, bool T, bool U, int Dep = kDepDirect>
 __global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const __grid_constant__ KernelArgs A) {
-  flight_body<R, G, D, T, U, Abs, Dep>(A);
+  flight_body<R, G, D, T, U, Dep>(A);
 }
 
 #if VMC_REAL_IS_FLOAT
-// absorb_mode: the launch's KernelArgs::absorb_mode; the BASELINE workloads'
-// production variants are compiled for their mode (see flight_body's kAbs).
 // dep: deposit path (kDepDirect / kDepWarp / kDepHotBox, see flight.cuh); the
-// aggregated paths exist for the production variants only (nullptr otherwise)
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int absorb_mode, int dep) {
+// aggregated paths exist for the production variants of the BASELINE
+// workloads only (nullptr otherwise)
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep) {
   using R = float;
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
   if (dep == kDepWarp) {
-    if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, 0, kDepWarp>);
-    if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, 0, kDepWarp>);
-    if (absorb_mode == 1 && !uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false, 1, kDepWarp>);
+    if (uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, kDepWarp>);
+    if (!uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, kDepWarp>);
+    if (!uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false, kDepWarp>);
     return nullptr;
   }
   if (dep == kDepHotBox) {
-    if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, 0, kDepHotBox>);
-    if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, 0, kDepHotBox>);
+    if (uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, kDepHotBox>);
+    if (!uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, kDepHotBox>);
     return nullptr;
   }
-  if (absorb_mode == 0 && uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, 0>);
-  if (absorb_mode == 0 && !uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, 0>);
-  if (absorb_mode == 1 && !uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false, 1>);
 #define VMC_FK(k, U)                                                                     \
   case k:                                                                                \
     return reinterpret_cast<const void*>(&k_flight<R, (k & 4) != 0, (k & 2) != 0, (k & 1) != 0, U>);

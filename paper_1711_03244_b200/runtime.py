@@ -523,7 +523,7 @@ class Plan:
 
     @property
     def kernel(self) -> str:
-        """Readable variant key: 'k_flight<float,G,D,T,U,Abs>' (or k_transport<...>)."""
+        """Readable variant key: 'k_flight<float,G,D,T,U,Dep>' (or k_transport<...>)."""
         return demangle_kernel(self.kernel_name)
 
     def close(self) -> None:
@@ -539,7 +539,7 @@ class Plan:
 
 
 def demangle_kernel(mangled: str) -> str:
-    """_ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi1EEEvNS_10KernelArgsE -> k_flight<float,1,0,0,0,1>
+    """_ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi0EEEvNS_10KernelArgsE -> k_flight<float,1,0,0,0,0>
     (the two kernel templates' Itanium manglings, decoded without c++filt)."""
     import re
     m = re.match(r"_ZN3vmc(\d+)(k_flight|k_transport)I([fd])((?:L[bi]n?\d+E)+)E", mangled or "")

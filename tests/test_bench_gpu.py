@@ -37,7 +37,7 @@ def test_bench_single_gpu_line(gpu):
     # per step: transport + replica fold + the record sort's key/gather kernels
     assert line["gpu_launches"] >= 3 * 2
     assert line["roofline"]["bound"] == "fp32" and 0 < line["roofline"]["frac"] < 1
-    assert line["roofline"]["kernel"] == "k_flight<float,0,1,0,0,0,0>"  # the B3 production variant
+    assert line["roofline"]["kernel"] == "k_flight<float,0,1,0,0,0>"  # the B3 production variant
     assert line["scaling"] == "strong" and "configs[4]" in line["config"]["workload"]
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
     assert line["cpu_baseline"]["cpu_model"]

@@ -1,12 +1,12 @@
 """Parity of the production kernel variants the bench lines time, at the
 BASELINE sizes (run with -m gpu on a B200).
 
-* head: 256^3 x 5 labels x 10 gates dispatches k_flight<float,1,0,0,0,1,0>
-  (gated, multi-label, Taylor-5 absorb compiled in). Its map is checked
-  against the compiled reference's gated walk (oracle/ref_capi.cpp ref_walk,
-  which re-drives transport.cpp:161-225 with a gate sink) and bit for bit
-  against the generic variant (absorb series picked at run time), whose trace
-  instantiation is then held photon by photon to the reference's RNG stream.
+* head: 256^3 x 5 labels x 10 gates dispatches k_flight<float,1,0,0,0,0>
+  (gated, multi-label, direct deposits). Its map is checked against the
+  compiled reference's gated walk (oracle/ref_capi.cpp ref_walk, which
+  re-drives transport.cpp:161-225 with a gate sink), and its trace
+  instantiation (same body, same arithmetic) photon by photon against the
+  reference's RNG stream.
 * B1 at BASELINE's own N = 1e6 with SURVEY §8(c)'s 1e-4 absorbed-fraction gate.
 """
 import numpy as np
@@ -40,7 +40,7 @@ def head_ref(ref, head256):
 def test_head256_dispatches_production_variant(gpu, head256):
     p = gpu.Plan(head256.scene, head256.config)
     try:
-        assert p.kernel == "k_flight<float,1,0,0,0,1,0>", p.kernel
+        assert p.kernel == "k_flight<float,1,0,0,0,0>", p.kernel
     finally:
         p.close()
 
@@ -74,23 +74,8 @@ def test_head256_run_parity(gpu, golden, head256, head_ref):
     assert e0 <= 1e-2 and e1 <= 5e-2, (e0, e1)
 
 
-def test_head256_production_equals_generic_variant(gpu, monkeypatch, head256):
-    """Compiled-in Taylor-5 (kAbs=1) and the run-time absorb dispatch of the
-    generic variant (kAbs=-1, absorb_mode 1) execute the same arithmetic: maps,
-    gates and dispositions bit for bit."""
-    st = head256
-    a = gpu.run_group_dynamic(0, 20_000, 1, st.scene, st.config)
-    monkeypatch.setenv("VMC_GENERIC_ABSORB", "1")
-    p = gpu.Plan(st.scene, st.config)
-    assert p.kernel == "k_flight<float,1,0,0,0,-1,0>", p.kernel
-    p.close()
-    b = gpu.run_group_dynamic(0, 20_000, 1, st.scene, st.config)
-    assert np.array_equal(a.map.cells, b.map.cells)
-    assert a.totals_q == b.totals_q
-
-
 def test_head256_per_photon_draws(gpu, ref, head256):
-    """The trace instantiation of the gated head kernel (generic absorb, same
+    """The trace instantiation of the gated head kernel (same body and
     arithmetic as production) photon by photon against the reference walk."""
     st = head256
     n = 20_000
@@ -129,7 +114,7 @@ def test_b1_at_baseline_size(gpu, ref, golden):
     n = 1_000_000
     st = v.baseline_setup("b1", photons=n, seed=1)
     p = gpu.Plan(st.scene, st.config)
-    assert p.kernel == "k_flight<float,0,0,0,1,0,0>", p.kernel
+    assert p.kernel == "k_flight<float,0,0,0,1,0>", p.kernel
     p.close()
     gold = golden["workloads"]["b1_1e6"]
     w = ref.walk(st.scene, st.config, 0, n, threads=8, cells=True, counts=True)
@@ -148,8 +133,8 @@ def test_b1_at_baseline_size(gpu, ref, golden):
     assert (x, y) == (30, 30) and z < 5
 
 
-@pytest.mark.parametrize("name,kernel", [("b2", "k_flight<float,0,0,0,1,0,0>"),
-                                         ("b3", "k_flight<float,0,1,0,0,0,0>")])
+@pytest.mark.parametrize("name,kernel", [("b2", "k_flight<float,0,0,0,1,0>"),
+                                         ("b3", "k_flight<float,0,1,0,0,0>")])
 def test_bench_variants_dispatch(gpu, name, kernel):
     """The variants the B2 / B3 bench lines time are the ones the run-parity
     tests of test_gpu_parity.py exercise (same scene, same selection)."""
