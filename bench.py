@@ -425,24 +425,26 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                     pkey, "profiles/roofline_traffic.json"))
         except Exception:
             pass
-    # secondary: L2 atomics. Red requests per photon MEASURED by ncu
-    # (lts__t_requests_op_red, profiles/roofline_traffic.json) at this kernel's
-    # photon rate, against the measured red.global.add.u64 rate of the
-    # workload's deposit-address distribution (tools/atomics_roofline.py)
-    reds = pj.get("issue", {}).get(pkey, {}).get("l2_red_requests_per_photon")
-    rate_basis = "ncu lts__t_requests_op_red per photon (profiles/roofline_traffic.json)"
+    # secondary: L2 atomics. Lanes that issued a red.global.add.u64 per photon,
+    # MEASURED by ncu (l1tex red sectors; the L2 request counter reads 1.5x that
+    # on B200, profiles/README.md), at this kernel's photon rate, against the
+    # measured red rate of the workload's deposit-address distribution
+    # (tools/atomics_bench: the B1 deposit addresses into 8 replicas; uniform
+    # addresses for the head map)
+    reds = pj.get("issue", {}).get(pkey, {}).get("red_lanes_per_photon")
+    rate_basis = "ncu l1tex__t_sectors_pipe_lsu_mem_global_op_red per photon (profiles/roofline_traffic.json)"
     if reds is None:
         reds, rate_basis = RUNS_PER_PHOTON[args.workload], "SURVEY §8(d) deposit runs per photon (unmeasured)"
-    l2 = {"achieved": reds * mine / (kern_ms_per * 1e-3), "unit": "red requests/s", "per_photon": reds,
+    l2 = {"achieved": reds * mine / (kern_ms_per * 1e-3), "unit": "red.add.u64 lanes/s", "per_photon": reds,
           "achieved_basis": rate_basis}
-    aprof = os.path.join(ROOT, "profiles", "atomics_roofline.json")
+    aprof = os.path.join(ROOT, "profiles", "r1_atomics_roofline.json")
     if os.path.exists(aprof):
         try:
             with open(aprof) as f:
                 aj = json.load(f)
-            key = aj.get("workload_key", {}).get(pkey, "uniform")
+            key = "uniform" if args.workload == "head" else "replay_rep8"
             l2.update(peak=aj[key], frac=l2["achieved"] / aj[key],
-                      peak_basis=f"profiles/atomics_roofline.json[{key}] (tools/atomics_bench on a B200)")
+                      peak_basis=f"profiles/r1_atomics_roofline.json[{key}] (tools/atomics_bench on a B200)")
         except Exception:
             pass
     roof["secondary"]["l2_atomics"] = l2
