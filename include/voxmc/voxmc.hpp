@@ -233,6 +233,40 @@ struct PhotonDisposition {
   }
 };
 
+// ---- single-photon state and host helpers (reference transport.hpp:16-83) --
+// The walk itself runs on the device (simulate_photon below, the executors);
+// these scalar helpers give reference callers the same one-photon building
+// blocks (launch state, DDA distance, one HG deflection, one roulette draw) on
+// the host, e.g. for tests and diagnostics. They are not used by any executor.
+struct PhotonState {
+  Vec3 position;
+  Vec3 direction;
+  Vec3 inv_direction;
+  double weight = 1.0;
+  double time_ns = 0.0;
+  double remaining_scat = 0.0;
+  std::uint8_t medium = 0;
+  VoxelIndex voxel;
+  void set_direction(const Vec3& d);
+};
+
+enum class StepKind { Scattered, CrossedVoxel, ExitedDomain, Reflected, Terminated };
+
+struct StepOutcome {
+  StepKind kind = StepKind::Terminated;
+  double deposited = 0.0;
+  bool interface_pending = false;
+  int face_axis = -1;
+  int face_step = 0;
+  VoxelIndex next_voxel;
+  bool next_is_exterior = false;
+};
+
+PhotonState launch(const Source& source, const VoxelGrid& grid, RngStream& stream);
+double distance_to_voxel_boundary(const Vec3& position, const Vec3& direction, const VoxelGrid& grid);
+Vec3 hg_scatter(const Vec3& direction, double g, RngStream& stream);
+bool roulette(PhotonState& photon, const SimulationConfig& config, RngStream& stream);
+
 // One photon's walk (reference transport.hpp:105-113), executed on CUDA device
 // 0 by the FP64 flight kernel (the reference's arithmetic): simulate_photon
 // adds every step deposit to `map` through FluenceMap::deposit;

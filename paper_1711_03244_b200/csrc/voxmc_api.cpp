@@ -5,6 +5,7 @@
 // the device through vmc_run_range / vmc_run_multi. Error codes from the C-ABI
 // are rethrown as the reference's exception types.
 #include <algorithm>
+#include <limits>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -200,6 +201,90 @@ double fresnel_reflectance(double n1, double n2, double ci) {
   const double rs = (n1 * ci - n2 * ct) / (n1 * ci + n2 * ct);
   const double rp = (n1 * ct - n2 * ci) / (n1 * ct + n2 * ci);
   return 0.5 * (rs * rs + rp * rp);
+}
+
+// ---- one-photon host helpers (reference transport.hpp:45-83, transport.cpp) --
+namespace {
+constexpr double kInfD = std::numeric_limits<double>::infinity();
+double unit_length(RngStream& stream) {  // -ln(u), u = 0 -> denorm_min (transport.cpp:14-17)
+  const double u = stream.next_unit();
+  return -std::log(u > 0.0 ? u : std::numeric_limits<double>::denorm_min());
+}
+}  // namespace
+
+void PhotonState::set_direction(const Vec3& d) {  // transport.cpp:77-81
+  direction = d;
+  inv_direction = {d.x != 0.0 ? 1.0 / d.x : kInfD, d.y != 0.0 ? 1.0 / d.y : kInfD, d.z != 0.0 ? 1.0 / d.z : kInfD};
+}
+
+PhotonState launch(const Source& source, const VoxelGrid& grid, RngStream& stream) {  // transport.cpp:83-106
+  Vec3 dir = source.direction.normalized();
+  if (source.isotropic) {
+    const double mu = 2.0 * stream.next_unit() - 1.0;
+    const double phi = 2.0 * 3.14159265358979323846 * stream.next_unit();
+    const double s = std::sqrt(std::max(0.0, 1.0 - mu * mu));
+    dir = {s * std::cos(phi), s * std::sin(phi), mu};
+  }
+  PhotonState st;
+  st.set_direction(dir);
+  st.position = source.position + dir * 1e-6;
+  const std::optional<VoxelIndex> v = grid.voxel_of(st.position);
+  if (!v) throw SourceOutsideDomain("source entry point maps outside the voxel grid");
+  st.voxel = *v;
+  st.medium = grid.label(*v);
+  st.remaining_scat = unit_length(stream);
+  return st;
+}
+
+double distance_to_voxel_boundary(const Vec3& position, const Vec3& direction, const VoxelGrid& grid) {
+  const std::optional<VoxelIndex> v = grid.voxel_of(position);  // transport.cpp:108-118, :49-73
+  if (!v) throw VoxelOutOfRange("position outside grid");
+  PhotonState st;
+  st.position = position;
+  st.set_direction(direction);
+  const int iv[3] = {v->x, v->y, v->z};
+  double best = kInfD;
+  for (int k = 0; k < 3; ++k) {
+    if (direction[k] == 0.0) continue;  // a zero component never crosses its planes
+    const double plane = (iv[k] + (direction[k] > 0.0 ? 1 : 0)) * grid.voxel_size();
+    const double t = std::max(0.0, (plane - position[k]) * st.inv_direction[k]);
+    if (t < best) best = t;  // strict: ties keep the lower axis
+  }
+  return best;
+}
+
+Vec3 hg_scatter(const Vec3& direction, double g, RngStream& stream) {  // transport.cpp:126-147
+  const double ct = hg_cos_theta(g, stream.next_unit());
+  const double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
+  double cp = 0.0, sp = 0.0;
+  for (;;) {  // uniform azimuth by rejection from the unit disk (transport.cpp:32-44)
+    const double ax = 2.0 * stream.next_unit() - 1.0;
+    const double ay = 2.0 * stream.next_unit() - 1.0;
+    const double r2 = ax * ax + ay * ay;
+    if (r2 > 1e-12 && r2 <= 1.0) {
+      const double k = 1.0 / std::sqrt(r2);
+      cp = ax * k;
+      sp = ay * k;
+      break;
+    }
+  }
+  const Vec3& d = direction;
+  Vec3 o;
+  if (std::fabs(d.z) > 0.99999) {
+    o = {st * cp, st * sp, d.z > 0.0 ? ct : -ct};
+  } else {
+    const double den = std::sqrt(1.0 - d.z * d.z);
+    o = {st * (d.x * d.z * cp - d.y * sp) / den + d.x * ct, st * (d.y * d.z * cp + d.x * sp) / den + d.y * ct,
+         -st * cp * den + d.z * ct};
+  }
+  const double n2 = o.dot(o);
+  return std::fabs(n2 - 1.0) > 1e-12 ? o * (1.0 / std::sqrt(n2)) : o;
+}
+
+bool roulette(PhotonState& photon, const SimulationConfig& config, RngStream& stream) {  // transport.cpp:300-306
+  if (!(stream.next_unit() < 1.0 / config.roulette_multiplier)) return false;
+  photon.weight *= config.roulette_multiplier;
+  return true;
 }
 
 // ---- FluenceMap -------------------------------------------------------------

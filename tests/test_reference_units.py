@@ -1,11 +1,13 @@
 """The reference's own doctest unit files (proj/tests/test_{rng,fluence,domain,
-scheduler}.cpp), compiled UNMODIFIED against the B200 drop-in headers
+scheduler,transport}.cpp), compiled UNMODIFIED against the B200 drop-in headers
 (include/voxmc) with the doctest stand-in tests/cpp/doctest.h and linked to
 libvoxmc_b200.so (recipe: oracle/Makefile `reftests`, built by
 __graft_entry__.build() where /root/reference exists; the binaries travel with
-the repo snapshot). Host-side units run here; test_scheduler's executor cases
-(run_group_dynamic / run_static_split / run_multi_device on the GPU) run with
--m gpu."""
+the repo snapshot). Host-side units run here; the executor cases of
+test_scheduler (run_group_dynamic / run_static_split / run_multi_device) and
+test_transport (simulate_photon_trace: Beer-Lambert, horizon, per-photon
+accounting to 1e-9, chord lengths to 1e-9, per-voxel path lengths against the
+ray-march oracle, reproducibility) run on the B200 with -m gpu."""
 import os
 import subprocess
 
@@ -36,6 +38,25 @@ def test_reference_scheduler_host_cases(filt):
     rc, out = run_unit("test_scheduler", filt)
     assert rc == 0, out[-3000:]
     assert "test cases: 0 " not in out  # the filter matched something
+
+
+@pytest.mark.parametrize("filt", ["pencil launch", "launch outside", "isotropic launch", "distance to voxel",
+                                  "boundary distance agrees", "Henyey-Greenstein median", "sample mean equals g",
+                                  "g = 0", "unit-norm over many", "Fresnel", "roulette"])
+def test_reference_transport_host_cases(filt):
+    """test_transport.cpp's host-side cases: launch state, DDA distance, HG
+    sampling statistics (1e6 deflections), Fresnel, roulette (1e6 draws)."""
+    rc, out = run_unit("test_transport", filt)
+    assert rc == 0, out[-3000:]
+    assert "test cases: 0 " not in out
+
+
+@pytest.mark.gpu
+def test_reference_transport_unit_on_gpu(gpu):
+    """All of test_transport.cpp, its walk cases through the device."""
+    rc, out = run_unit("test_transport")
+    assert rc == 0, out[-3000:]
+    assert " 0 failed" in out
 
 
 @pytest.mark.gpu
