@@ -44,9 +44,23 @@ def corner_scene(kind):
         grid = v.VoxelGrid((nx, ny, nz), 0.37, lab, media)
         src = v.Source((17 * 0.37 / 2, 23 * 0.37 / 2, 0.0), (0.1, 0.05, 1.0))
         return v.Scene(grid, src), cfg
+    elif kind == "mosaic":  # 2x2x2-voxel blocks of 5 random media (4 refractive indices): interfaces
+        # in every direction, Fresnel / TIR / refraction on most faces
+        rng = np.random.default_rng(17)
+        blocks = rng.integers(1, 6, (n // 2, n // 2, n // 2)).astype(np.uint8)
+        lab = np.repeat(np.repeat(np.repeat(blocks, 2, 0), 2, 1), 2, 2)
+        media = [air, v.OpticalProperties(0.01, 1.0, 0.8, 1.37), v.OpticalProperties(0.02, 2.0, 0.5, 1.0),
+                 v.OpticalProperties(0.005, 0.5, 0.9, 1.45), v.OpticalProperties(0.03, 4.0, 0.0, 1.33),
+                 v.OpticalProperties(0.01, 1.5, -0.3, 1.37)]
+    elif kind == "iso_layers":  # isotropic point source inside layered media of different n
+        media = [air, v.OpticalProperties(0.01, 1.0, 0.9, 1.37), v.OpticalProperties(0.02, 3.0, 0.7, 1.45),
+                 v.OpticalProperties(0.005, 0.2, 0.0, 1.33)]
+        z = np.arange(n)[:, None, None] * np.ones((1, n, n), np.int64)
+        lab = np.where(z < 7, 1, np.where(z < 13, 2, 3)).astype(np.uint8)
+        src = v.Source((9.7, 10.3, 10.1), (0.0, 0.0, 1.0), isotropic=True)
     grid = v.VoxelGrid((n, n, n), 1.0, lab, media)
     return v.Scene(grid, src), cfg
 
 
 CORNERS = ["roulette", "horizon", "backward", "dense_inclusion", "terminate_inner", "oblique", "ballistic",
-           "aniso_grid"]
+           "aniso_grid", "mosaic", "iso_layers"]
