@@ -438,6 +438,13 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   // measured: 70-80 flat, 75 best by 0.3 %; clamped so a warp always walks while >= 1 lane of 32 does
   A.event_pct = std::min(100, std::max(4, env_int("VMC_EVENT_PCT", 75)));
   A.walk_keep = (32 * (100 - A.event_pct)) / 100;
+  {
+    // scatter chain for strongly scattering volumes (max mus * h >= 10: most
+    // flights end in their voxel); VMC_SCATTER_CHAIN overrides the lane count
+    double mx = 0.0;
+    for (int m = 0; m < s->nmedia; ++m) mx = std::max(mx, s->media[4 * m + 1] * s->voxel_mm);
+    A.chain_min = std::max(0, std::min(32, env_int("VMC_SCATTER_CHAIN", mx >= 10.0 ? 22 : 0)));
+  }
   // K1f (flight.cuh) in the launch's precision unless VMC_KERNEL=step selects
   // the per-step K1 (transport.cuh) for A/B runs. FP64 K1f is the
   // exact-arithmetic pin of the product kernel's structure.

@@ -128,7 +128,7 @@ struct KernelArgs {
   int pad10, pad7;
   float detf[kMaxDet][4];  // K1f: detector disks as {x, y, z, r^2} in FP32
   int hb0[3];              // K1f hot-box deposits: box origin voxel (16^3 box around the source)
-  int pad12;
+  int chain_min;  // K1f scatter chain: >= chain_min lanes ending their new flight in-voxel (0 = off)
 };
 
 
