@@ -489,9 +489,11 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     if (cudaFuncGetName(&nm, P->kern) == cudaSuccess && nm) P->kern_name = nm;
     else cudaGetLastError();
   }
-  // media table, plus per-thread per-label path lengths in detector mode
+  // media table, plus per-thread per-label path lengths in detector mode (one
+  // slot per interior label; K1 and K1f both place them after the media)
   P->smem = ((media_bytes + 15) & ~static_cast<size_t>(15)) +
-            (det ? static_cast<size_t>(vmc::kMaxDetMedia) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float)) : 0);
+            (det ? static_cast<size_t>(std::max(1, s->nmedia - 1)) * vmc::kBlock * (f64 ? sizeof(double) : sizeof(float))
+                 : 0);
   // K1f adds its per-thread disposition slots and per-warp seed stashes (the
   // kernel places them at compile-time offsets in front of the media table)
   P->smem = ((P->smem + 15) & ~static_cast<size_t>(15)) + 3 * vmc::kBlock * sizeof(long long) +

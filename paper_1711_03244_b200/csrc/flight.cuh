@@ -148,15 +148,17 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   constexpr int WALK = 0, SCAT = 1, DEAD = 2, RETRY = 3, FACE = 4, SETUP = 5, ENDF = 6;
   unsigned char* smem = vmc_smem;
   // Shared-memory layout at compile-time offsets (cheap to rematerialise):
-  // per-thread disposition slots | per-warp seed stashes | per-thread path
-  // lengths (detector kernels) | media table
+  // per-thread disposition slots | per-warp seed stashes | [hot box] | media
+  // table | per-thread path lengths (detector kernels, after the media)
   constexpr int kStashBytes = flight_stash_bytes(sizeof(Real));
   constexpr int kAccOff = 0;                                       // 3 x kBlock x int64
   constexpr int kStashOff = kAccOff + 3 * kBlock * 8;              // kBlock / 32 x kStashBytes
-  constexpr int kPpOff = kStashOff + (kBlock / 32) * kStashBytes;
-  constexpr int kHbOff = kPpOff + (kDet ? kMaxDetMedia * kBlock * static_cast<int>(sizeof(Real)) : 0);
+  constexpr int kHbOff = kStashOff + (kBlock / 32) * kStashBytes;
   constexpr int kMediaOff = kHbOff + (kDep == kDepHotBox ? kHotBoxBytes : 0);
-  static_assert(kStashOff % 16 == 0 && kPpOff % 16 == 0 && kMediaOff % 16 == 0, "smem alignment");
+  static_assert(kStashOff % 16 == 0 && kHbOff % 16 == 0 && kMediaOff % 16 == 0, "smem alignment");
+  // detector kernels: per-thread per-label path lengths after the media table,
+  // sized by the volume's interior labels (nppath x kBlock), not the maximum,
+  // so the L1 keeps the rest of the SM's 256 KB for the label volume
   static_assert(kDep != kDepHotBox || !kGates, "the hot box serves ungated kernels");
   constexpr int kHbCells = kHotBoxN * kHotBoxN * kHotBoxN;
   unsigned* const hb_lo = reinterpret_cast<unsigned*>(smem + kHbOff);
@@ -233,7 +235,10 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   uint32_t steps = 0, nscat = 0;
   double pd_dep = 0, pd_esc = 0, pd_kill = 0, pd_trunc = 0;  // trace only
   bool detected = false;
-  Real* pp_sm = reinterpret_cast<Real*>(smem + kPpOff) + threadIdx.x;
+  Real* pp_sm = reinterpret_cast<Real*>(
+                    smem + kMediaOff + ((static_cast<int>(sizeof(Medium<Real>)) * A.nmedia + 15) & ~15)) +
+                threadIdx.x;
+  Real seg = 0;  // detector kernels: path length in the current medium since the last flush
 
   auto quant = [&](Real x) -> long long { return F::quant(x, qscale); };
   auto gate_of = [&](Real tt) -> int {
@@ -371,9 +376,17 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
     return false;
   };
+  // detector kernels: path length in the current medium accumulates in a
+  // register and goes to this thread's per-label slot in shared memory only
+  // when the label changes or the photon exits (B3: ~3.5 label changes against
+  // ~160 flight segments per photon)
   auto add_path = [&](Real s) {
+    if constexpr (kDet) seg += s;
+  };
+  auto flush_path = [&]() {
     if constexpr (kDet) {
-      if (lab >= 1) pp_sm[(lab - 1) * kBlock] += s;
+      if (lab >= 1) pp_sm[(lab - 1) * kBlock] += seg;
+      seg = Real(0);
     }
   };
   auto scat_len = [&]() -> Real { return F::scat_len(rng); };
@@ -672,6 +685,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       acc_sm[0] += quant(w);
       if constexpr (kTrace) pd_esc += w;
       if constexpr (kDet) {
+        flush_path();
         int hit = -1;
         for (int k = 0; k < A.ndet; ++k) {
           // in the kernel's precision, like the exit position itself
@@ -729,6 +743,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
         dz = -dz;
       }
     } else {
+      if (nl != lab) flush_path();
       lab = nl;
     }
     tf = t;
@@ -801,6 +816,7 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if constexpr (kDet) {
       nscat = 0;
       for (int m = 0; m < A.nppath; ++m) pp_sm[m * kBlock] = Real(0);
+      seg = Real(0);
     }
     phase = SETUP;
   };
