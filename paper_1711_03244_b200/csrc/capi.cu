@@ -511,6 +511,23 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     if (cap > 0) per_sm = std::min(per_sm, cap);
   }
   P->grid = std::max(1, per_sm) * P->sms;
+  {
+    // Shared-memory carveout: just what the resident CTAs need, so the rest of
+    // the SM's L1/shared array caches the label volume (read through __ldg on
+    // every face of multi-label volumes). Left to itself the driver picked the
+    // 132 KB configuration for B3's 4 x 21 KB (ncu launch__shared_mem_config_size).
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    const int pct_env = env_int("VMC_SMEM_CARVEOUT", -1);
+    if (max_smem > 0 && pct_env != 0) {
+      const long need = static_cast<long>(std::max(1, per_sm)) * (static_cast<long>(P->smem) + 1024);
+      int pct = pct_env > 0 ? pct_env : static_cast<int>((need * 100 + max_smem - 1) / max_smem);
+      pct = std::max(1, std::min(100, pct));
+      cudaFuncSetAttribute(P->kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaGetLastError();
+    }
+  }
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern_trace, P->block, P->smem_trace), "occupancy");
   P->grid_trace = std::max(1, per_sm) * P->sms;
 
