@@ -289,6 +289,7 @@ struct vmc_plan {
   int block = vmc::kBlock;
   size_t smem = 0, smem_trace = 0;
   int grid = 0, grid_trace = 0;
+  bool grid_adaptive = true;  // launch-time grid by photons per thread (VMC_ADAPTIVE_GRID=0: off)
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
   std::string kern_name;  // mangled device symbol of `kern` (cudaFuncGetName)
@@ -509,6 +510,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   {
     const int cap = env_int("VMC_CTAS_PER_SM", 0);  // A/B knob: fewer resident CTAs per SM
     if (cap > 0) per_sm = std::min(per_sm, cap);
+    P->grid_adaptive = env_int("VMC_ADAPTIVE_GRID", 1) != 0 && cap <= 0;
   }
   P->grid = std::max(1, per_sm) * P->sms;
   {
@@ -629,7 +631,19 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   }
   // never launch more persistent threads than photons need
   const uint64_t need_blocks = (count + P->block - 1) / P->block;
-  const int full = trace ? P->grid_trace : P->grid;
+  int full = trace ? P->grid_trace : P->grid;
+  // Small runs: fewer resident CTAs per SM. With only a few photons per
+  // resident thread the run ends when the longest horizon-truncated photon
+  // chain does (~1150 dependent scatters in B1), and that chain advances
+  // faster on a less contended SM. Measured on B200 (profiles/README.md,
+  // "small photon counts"): of 4 CTAs/SM, 2 are best below ~7 photons per
+  // full-grid thread (B1 at 1e6: +19 %), 3 below ~30, all 4 above.
+  if (!trace && P->grid_adaptive && full >= 4 * P->sms) {
+    const int per = full / P->sms;
+    const double r = static_cast<double>(count) / (static_cast<double>(full) * P->block);
+    const int c = r < 7.0 ? per / 2 : (r < 30.0 ? per - per / 4 : per);
+    full = c * P->sms;
+  }
   const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));
   {
     void* argv[] = {&A};

@@ -202,6 +202,23 @@ def test_map_replicas_bit_identical(gpu, monkeypatch, name):
         assert x.det_count == runs[0].det_count
 
 
+@pytest.mark.parametrize("name,n", [("b1", 200_000), ("b1", 1_000_000), ("b3", 1_500_000)])
+def test_adaptive_grid_bit_identical(gpu, monkeypatch, name, n):
+    """Small runs launch fewer resident CTAs per SM (2 or 3 of 4 below 7 / 30
+    photons per full-grid thread); which lane carries a photon never changes
+    its result: maps, dispositions and detector records equal the full grid's."""
+    st = setup(name, n=n)
+    runs = []
+    for on in ("0", "1"):
+        monkeypatch.setenv("VMC_ADAPTIVE_GRID", on)
+        runs.append(gpu.run_group_dynamic(0, n, 1, st.scene, st.config))
+    full, adaptive = runs
+    assert np.array_equal(adaptive.map.cells, full.map.cells) and adaptive.totals_q == full.totals_q
+    assert adaptive.det_count == full.det_count
+    if full.detections is not None:
+        assert np.array_equal(adaptive.detections, full.detections)
+
+
 @pytest.mark.parametrize("name,modes", [("b1", ("warp", "hotbox")), ("b2", ("warp", "hotbox")),
                                         ("b3", ("warp", "hotbox")), ("head", ("warp",))])
 def test_deposit_paths_bit_identical(gpu, monkeypatch, name, modes):

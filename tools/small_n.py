@@ -3,8 +3,10 @@ run_group_dynamic call and its wall time (host buffers), best of 3."""
 import sys, time
 sys.path.insert(0, ".")
 import paper_1711_03244_b200 as v
-for name in ("b1", "b2"):
-    for n in (100_000, 1_000_000, 10_000_000, 100_000_000):
+SIZES = {"b1": (100_000, 1_000_000, 10_000_000, 100_000_000), "b2": (100_000, 1_000_000, 10_000_000, 100_000_000),
+         "b3": (100_000, 1_000_000, 10_000_000, 100_000_000), "head": (100_000, 1_000_000, 10_000_000)}
+for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ("b1", "b2")):
+    for n in SIZES[name]:
         st = v.baseline_setup(name, photons=n)
         best_dev, best_wall = 1e30, 1e30
         for _ in range(3):
