@@ -1,8 +1,7 @@
 """Small-N tail probe: how long do the longest photons of a run take on their
-own? Traces N photons of a workload, picks the ones with the most scatters,
-and times device runs of just those photons (1 photon; the 32 longest in one
-warp each, i.e. 32 separate one-photon ranges launched back to back is not
-what we want — a range of the longest photon alone, then the full run).
+own? Traces N photons of a workload, picks the three with the most scatters,
+times a one-photon run of each (the latency floor of the run's tail), then the
+full N-photon run.
 usage: python tools/tail_probe.py b1 1e6
 """
 import sys
