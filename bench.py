@@ -500,9 +500,11 @@ def main():
         import torch
         import torch.distributed as dist
         # NCCL's init log ("comm ... rank r nranks N ... Init COMPLETE", one per
-        # rank) stays on: it is how a reader counts the ranks that joined
+        # rank) stays on, on stderr: it is how a reader counts the ranks that
+        # joined, and stdout carries only rank 0's JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.backend == "nccl":

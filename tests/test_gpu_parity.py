@@ -202,15 +202,19 @@ def test_map_replicas_bit_identical(gpu, monkeypatch, name):
         assert x.det_count == runs[0].det_count
 
 
-@pytest.mark.parametrize("name,n", [("b1", 200_000), ("b1", 1_000_000), ("b3", 1_500_000)])
-def test_adaptive_grid_bit_identical(gpu, monkeypatch, name, n):
+@pytest.mark.parametrize("name,n", [("b1", 200_000), ("b1", 1_000_000), ("b3", 300_000), ("b3", 1_500_000),
+                                    ("head", 50_000)])
+def test_small_run_scheduling_bit_identical(gpu, monkeypatch, name, n):
     """Small runs launch fewer resident CTAs per SM (2 or 3 of 4 below 7 / 30
-    photons per full-grid thread); which lane carries a photon never changes
-    its result: maps, dispositions and detector records equal the full grid's."""
+    photons per full-grid thread), and a warp's last photon finishes in a
+    lane-local loop once the claims have run out. Neither changes what a
+    photon computes: maps, dispositions and detector records equal those of
+    the full grid with warp-synchronous scheduling to the end."""
     st = setup(name, n=n)
     runs = []
-    for on in ("0", "1"):
-        monkeypatch.setenv("VMC_ADAPTIVE_GRID", on)
+    for grid, solo in (("0", "0"), ("1", "1")):
+        monkeypatch.setenv("VMC_ADAPTIVE_GRID", grid)
+        monkeypatch.setenv("VMC_SOLO", solo)
         runs.append(gpu.run_group_dynamic(0, n, 1, st.scene, st.config))
     full, adaptive = runs
     assert np.array_equal(adaptive.map.cells, full.map.cells) and adaptive.totals_q == full.totals_q

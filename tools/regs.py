@@ -7,10 +7,12 @@ cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
 err = subprocess.run(cmd, capture_output=True, text=True).stderr
 cur = None
 for ln in err.split("\n"):
-    m = re.search(r"Compiling entry function '_ZN3vmc(\d+)(k_\w+?)I(\w+?)EEEvNS_10KernelArgsE'", ln)
+    m = re.search(r"Compiling entry function '_ZN3vmc(\d+)(k_\w+?)I(\w+?)EEvNS_10KernelArgsE'", ln)
     if m:
-        cur = m.group(2) + "<" + ",".join("1" if b == "1" else "0" for b in re.findall(r"Lb(\d)", m.group(3))) + ">"
-        if "Lf" in m.group(3): cur = cur.replace("<", "<f,")
+        args = m.group(3)
+        real = "float" if args.startswith("f") else ("double" if args.startswith("d") else "")
+        parts = [("1" if b == "1" else "0") for b in re.findall(r"Lb(\d)", args)] + re.findall(r"Li(\d+)E", args)
+        cur = m.group(2) + "<" + ",".join(([real] if real else []) + parts) + ">"
         continue
     m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", ln)
     if m and cur: spill = (m.group(1), m.group(2))
