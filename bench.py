@@ -499,12 +499,6 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        # NCCL's init log ("comm ... rank r nranks N ... Init COMPLETE", one per
-        # rank) stays on, on stderr: it is how a reader counts the ranks that
-        # joined, and stdout carries only rank 0's JSON line
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.backend == "nccl":
@@ -519,7 +513,7 @@ def main():
             import torch.distributed as dist
             dist.barrier()
             dist.destroy_process_group()
-    if line is not None:  # rank 0, after every rank's NCCL teardown log: the JSON line is last
+    if line is not None:  # rank 0, after every rank's teardown: the JSON line is the last stdout line
         if world > 1:
             time.sleep(0.5)
         print(json.dumps(line), flush=True)

@@ -24,6 +24,10 @@ print(f"{name} N={n}: scatters mean {sc.mean():.1f} p99 {np.percentile(sc, 99):.
       f"{np.percentile(sc, 99.9):.0f} max {sc.max()} (photon {order[0]})", flush=True)
 cells = torch.empty(plan.ncells, dtype=torch.int64, device="cuda")
 tot = torch.empty(4, dtype=torch.int64, device="cuda")
+det = det_n = None
+if st.config.detectors:
+    det = torch.empty(max(1, st.config.det_capacity) * plan.rec_bytes, dtype=torch.uint8, device="cuda")
+    det_n = torch.empty(1, dtype=torch.int64, device="cuda")
 
 
 def dev_ms(first, count, reps=3):
@@ -33,7 +37,7 @@ def dev_ms(first, count, reps=3):
         b = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record()
-        plan.run_torch(first, count, cells, tot)
+        plan.run_torch(first, count, cells, tot, det, det_n)
         b.record()
         torch.cuda.synchronize()
         best = min(best, a.elapsed_time(b))
