@@ -445,7 +445,6 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     double mx = 0.0;
     for (int m = 0; m < s->nmedia; ++m) mx = std::max(mx, s->media[4 * m + 1] * s->voxel_mm);
     A.chain_min = std::max(0, std::min(32, env_int("VMC_SCATTER_CHAIN", mx >= 10.0 ? 22 : 0)));
-    A.solo = std::max(0, std::min(32, env_int("VMC_SOLO", 1)));
   }
   // K1f (flight.cuh) in the launch's precision unless VMC_KERNEL=step selects
   // the per-step K1 (transport.cuh) for A/B runs. FP64 K1f is the

@@ -940,27 +940,6 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if (exhausted) {
       const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
       if (dead == 0xffffffffu) break;
-      if (A.solo) {
-        // The warp's last photon (small-N tail: typically a horizon-truncated
-        // one with ~1000 scatters left) runs to its end in a lane-local loop:
-        // no votes, no event-phase dispatch, nothing to batch with
-        if (32 - __popc(dead) <= A.solo) {
-          if (phase != DEAD) {
-            for (;;) {
-              if (phase == WALK) {
-                walk();
-                continue;
-              }
-              if (phase == ENDF) end_flight();
-              if (phase == SCAT || phase == RETRY) scatter();
-              if (phase == FACE) face();
-              if (phase == SETUP) setup();
-              if (phase == DEAD) break;
-            }
-          }
-          break;
-        }
-      }
       keep = ((32 - __popc(dead)) * A.walk_keep) >> 5;
     }
     // After an event phase nearly every lane walks in the cube60 kernels, so

@@ -119,7 +119,7 @@ struct KernelArgs {
   int pad11;
   float gate_wf;  // K1f: gate width tmax / ngates (FP32)
   int event_pct;
-  int solo;  // K1f: a warp's last photon after the claims run out finishes in a lane-local loop
+  int pad14;
   // fluence-map replicas: CTA b deposits into cells + (b & rep_mask) * rep_stride
   // (the host folds the replicas into the caller's map after the launch)
   long long rep_stride;
