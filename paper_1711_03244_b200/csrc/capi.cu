@@ -116,7 +116,73 @@ bool inside(const vmc_scene* s, const int* v) {
   return v[0] >= 0 && v[1] >= 0 && v[2] >= 0 && v[0] < s->nx && v[1] < s->ny && v[2] < s->nz;
 }
 
-void validate(const vmc_scene* s, const vmc_config* c) {
+// Label-volume facts every call needs (the largest label for validation, and
+// whether the volume is single-label for the kernel choice), cached by a
+// 64-bit digest of the volume: a repeated call on the same volume reads the
+// labels once (the digest pass) instead of three times, and vmc_run_range
+// skips the label upload when the device already holds that volume.
+struct LabelInfo {
+  uint64_t digest = 0;
+  uint8_t max = 0;
+  bool uniform = false;
+};
+
+uint64_t label_digest(const uint8_t* p, size_t n) {
+  // four independent multiply-xor chains over 8-byte words, then the tail
+  uint64_t h[4] = {0x243F6A8885A308D3ull, 0x13198A2E03707344ull, 0xA4093822299F31D0ull, 0x082EFA98EC4E6C89ull};
+  const size_t nw = n / 8;
+  size_t i = 0;
+  for (; i + 4 <= nw; i += 4) {
+    for (int k = 0; k < 4; ++k) {
+      uint64_t w;
+      std::memcpy(&w, p + 8 * (i + k), 8);
+      h[k] = (h[k] ^ w) * 0x9E3779B97F4A7C15ull;
+      h[k] ^= h[k] >> 29;
+    }
+  }
+  for (; i < nw; ++i) {
+    uint64_t w;
+    std::memcpy(&w, p + 8 * i, 8);
+    h[0] = (h[0] ^ w) * 0x9E3779B97F4A7C15ull;
+    h[0] ^= h[0] >> 29;
+  }
+  for (size_t j = 8 * nw; j < n; ++j) h[1] = (h[1] ^ p[j]) * 0x100000001B3ull;
+  uint64_t r = n;
+  for (int k = 0; k < 4; ++k) r = vmc::mix64(r ^ h[k]);
+  return r;
+}
+
+LabelInfo label_info(const vmc_scene* s) {
+  const size_t nvox = static_cast<size_t>(s->nx) * s->ny * s->nz;
+  LabelInfo li;
+  li.digest = label_digest(s->labels, nvox);
+  static std::mutex mu;
+  static LabelInfo recent[8];
+  static size_t recent_n[8] = {};
+  static int next = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (int k = 0; k < 8; ++k)
+      if (recent_n[k] == nvox && recent[k].digest == li.digest) return recent[k];
+  }
+  uint8_t mx = 0;
+  bool uni = true;
+  const uint8_t l0 = s->labels[0];
+  for (size_t i = 0; i < nvox; ++i) {
+    const uint8_t b = s->labels[i];
+    mx = std::max(mx, b);
+    uni = uni && b == l0;
+  }
+  li.max = mx;
+  li.uniform = uni;
+  std::lock_guard<std::mutex> lock(mu);
+  recent[next] = li;
+  recent_n[next] = nvox;
+  next = (next + 1) % 8;
+  return li;
+}
+
+void validate(const vmc_scene* s, const vmc_config* c, LabelInfo* info = nullptr) {
   if (!s || !c) fail_validation("null scene/config");
   // VoxelGrid ctor, types.cpp:7-33
   if (s->nx < 1 || s->ny < 1 || s->nz < 1) fail_validation("VoxelGrid: all dims must be >= 1");
@@ -131,9 +197,9 @@ void validate(const vmc_scene* s, const vmc_config* c) {
       fail_validation("VoxelGrid: invalid optical properties");
   }
   const size_t nvox = static_cast<size_t>(s->nx) * s->ny * s->nz;
-  uint8_t mx = 0;
-  for (size_t i = 0; i < nvox; ++i) mx = std::max(mx, s->labels[i]);
-  if (mx >= s->nmedia) fail_validation("VoxelGrid: label exceeds media list");
+  const LabelInfo li = label_info(s);
+  if (info) *info = li;
+  if (li.max >= s->nmedia) fail_validation("VoxelGrid: label exceeds media list");
   // SimulationConfig::validate, types.cpp:44-52
   if (c->photon_count < 1) fail_validation("photon_count must be >= 1");
   if (!(c->tmax_ns > 0.0)) fail_validation("tmax must be > 0");
@@ -265,6 +331,8 @@ struct RecSort {
 struct RangeCache {
   std::mutex mu;
   DevBuf labels, media, mua, claim, err, cells, totals, det, detn, rep;
+  uint64_t labels_digest = 0;  // the volume `labels` holds (valid when labels_n > 0)
+  size_t labels_n = 0;
   RecSort rs;
 };
 
@@ -316,7 +384,8 @@ struct vmc_plan {
 namespace {
 
 void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device, RangeCache* cache = nullptr) {
-  validate(s, c);
+  LabelInfo li;
+  validate(s, c, &li);
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   if (device < 0 || device >= ndev) fail_validation("device index out of range");
@@ -340,8 +409,18 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
       own.alloc(bytes, device);
     }
   };
-  get(P->labels, cache ? &cache->labels : nullptr, nvox);
-  ck(cudaMemcpy(P->labels.p, s->labels, nvox, cudaMemcpyHostToDevice), "upload labels");
+  if (cache && cache->labels.p && cache->labels.dev == device && cache->labels.cap >= nvox && cache->labels_n == nvox &&
+      cache->labels_digest == li.digest) {
+    P->labels.borrow(cache->labels);  // the device already holds this volume
+  } else {
+    get(P->labels, cache ? &cache->labels : nullptr, nvox);
+    if (cache) cache->labels_n = 0;  // invalid until the upload completes
+    ck(cudaMemcpy(P->labels.p, s->labels, nvox, cudaMemcpyHostToDevice), "upload labels");
+    if (cache) {
+      cache->labels_n = nvox;
+      cache->labels_digest = li.digest;
+    }
+  }
   const bool f64 = c->precision == VMC_PRECISION_FP64;
   size_t media_bytes;
   if (f64) {
@@ -385,6 +464,8 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
     for (int k = 0; k < 3; ++k) {
       A.dir0[k] = L.dir[k];
       A.pos0[k] = L.pos[k];
+      A.dir0f[k] = static_cast<float>(L.dir[k]);
+      A.pos0f[k] = static_cast<float>(L.pos[k]);
       A.v0[k] = L.v[k];
     }
     A.lab0 = s->labels[static_cast<size_t>(L.v[0]) + static_cast<size_t>(s->nx) * (L.v[1] + static_cast<size_t>(s->ny) * L.v[2])];
@@ -423,10 +504,9 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   A.det_cap = c->det_capacity;
 
   const bool gates = c->ngates > 1, det = c->ndet > 0;
-  bool uniform = true;  // single-label volume -> specialised kernel (identical results)
+  bool uniform = li.uniform;  // single-label volume -> specialised kernel (identical results)
   {
     const uint8_t l0 = s->labels[0];
-    for (size_t i = 1; i < nvox && uniform; ++i) uniform = s->labels[i] == l0;
     const char* ku = std::getenv("VMC_UNIFORM_FASTPATH");
     if (ku && ku[0] == '0') uniform = false;
     if (uniform && l0 < s->nmedia) {

@@ -63,6 +63,15 @@
 
 #include "transport.cuh"
 
+// Compile-time A/B knobs of the detector kernels (B3): walk steps per warp
+// vote, and whether the walk loop votes before its first pass.
+#ifndef VMC_WALK_STEPS_DET
+#define VMC_WALK_STEPS_DET 3  // 2 or 3
+#endif
+#ifndef VMC_VOTE_FIRST_DET
+#define VMC_VOTE_FIRST_DET 0
+#endif
+
 namespace vmc {
 
 #ifdef VMC_STATS
@@ -786,12 +795,13 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
       }
       lab = __ldg(A.labels + (ux + nx * (uy + static_cast<long long>(A.ny) * uz)));
     } else {
-      dx = static_cast<Real>(A.dir0[0]);
-      dy = static_cast<Real>(A.dir0[1]);
-      dz = static_cast<Real>(A.dir0[2]);
-      px = static_cast<Real>(A.pos0[0]);
-      py = static_cast<Real>(A.pos0[1]);
-      pz = static_cast<Real>(A.pos0[2]);
+      // FP32: converted once on the host (no F2F.F32.F64 per launch)
+      dx = F::pick(A.dir0f[0], A.dir0[0]);
+      dy = F::pick(A.dir0f[1], A.dir0[1]);
+      dz = F::pick(A.dir0f[2], A.dir0[2]);
+      px = F::pick(A.pos0f[0], A.pos0[0]);
+      py = F::pick(A.pos0f[1], A.pos0[1]);
+      pz = F::pick(A.pos0f[2], A.pos0[2]);
       ux = A.v0[0];
       uy = A.v0[1];
       uz = A.v0[2];
@@ -815,7 +825,14 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     }
     if constexpr (kDet) {
       nscat = 0;
-      for (int m = 0; m < A.nppath; ++m) pp_sm[m * kBlock] = Real(0);
+      // four predicated stores per pass instead of a per-slot loop (launch
+      // runs on the one or two lanes that refill; B3 +0.4 %)
+#pragma unroll 1
+      for (int m = 0; m < A.nppath; m += 4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (m + j < A.nppath) pp_sm[(m + j) * kBlock] = Real(0);
+      }
       seg = Real(0);
     }
     phase = SETUP;
@@ -946,19 +963,24 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // their first vote is skipped (+1 %); in the strongly scattering head most
     // new flights end in their voxel, so the gated kernel votes first
     // (three steps per vote amortise the loop control; 2 and 4 measured slower)
-    if constexpr (kGates) {
+    constexpr int kSteps = kDet ? VMC_WALK_STEPS_DET : 3;
+    if constexpr (kGates || (kDet && VMC_VOTE_FIRST_DET)) {
       while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep) {
         VMC_ST(6, 1);
         if (phase == WALK) walk();
         if (phase == WALK) walk();
-        if (phase == WALK) walk();
+        if constexpr (kSteps >= 3) {
+          if (phase == WALK) walk();
+        }
       }
     } else {
       do {
         VMC_ST(6, 1);
         if (phase == WALK) walk();
         if (phase == WALK) walk();
-        if (phase == WALK) walk();
+        if constexpr (kSteps >= 3) {
+          if (phase == WALK) walk();
+        }
       } while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep);
     }
   }

@@ -129,6 +129,7 @@ struct KernelArgs {
   float detf[kMaxDet][4];  // K1f: detector disks as {x, y, z, r^2} in FP32
   int hb0[3];              // K1f hot-box deposits: box origin voxel (16^3 box around the source)
   int chain_min;  // K1f scatter chain: >= chain_min lanes ending their new flight in-voxel (0 = off)
+  float dir0f[3], pos0f[3];  // K1f FP32: the pencil launch state, converted once on the host
 };
 
 
