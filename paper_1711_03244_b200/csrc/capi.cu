@@ -33,7 +33,7 @@
 namespace vmc {
 const void* transport_kernel_float(bool gates, bool det, bool trace, bool uniform);
 const void* transport_kernel_double(bool gates, bool det, bool trace, bool uniform);
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep);
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep, bool solo = false);
 const void* flight_kernel_double(bool gates, bool det, bool trace, bool uniform);
 }  // namespace vmc
 
@@ -360,6 +360,7 @@ struct vmc_plan {
   bool grid_adaptive = true;  // launch-time grid by photons per thread (VMC_ADAPTIVE_GRID=0: off)
   const void* kern = nullptr;
   const void* kern_trace = nullptr;
+  const void* kern_solo = nullptr;  // small-run instantiation of `kern` (K1f FP32 production variants)
   std::string kern_name;  // mangled device symbol of `kern` (cudaFuncGetName)
   int dep = 0;            // deposit path of `kern` (vmc::kDepDirect / kDepWarp / kDepHotBox)
   // fluence-map scratch: nrep replicas (nrep > 1 for small maps) the transport
@@ -555,6 +556,8 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
       P->kern = vmc::flight_kernel_float(gates, det, false, uniform, vmc::kDepDirect);
     }
     P->kern_trace = vmc::flight_kernel_float(gates, det, true, uniform, vmc::kDepDirect);
+    if (P->dep == vmc::kDepDirect && env_int("VMC_SOLO", 1) != 0)
+      P->kern_solo = vmc::flight_kernel_float(gates, det, false, uniform, vmc::kDepDirect, true);
     if (P->dep == vmc::kDepHotBox) {
       // 16^3 box around the source voxel, clamped into the grid
       const int n3[3] = {s->nx, s->ny, s->nz};
@@ -585,6 +588,9 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
   ck(cudaFuncSetAttribute(P->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem_trace)),
      "smem attr");
+  if (P->kern_solo)
+    ck(cudaFuncSetAttribute(P->kern_solo, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)),
+       "smem attr");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P->kern, P->block, P->smem), "occupancy");
   {
@@ -607,6 +613,7 @@ void plan_init(vmc_plan* P, const vmc_scene* s, const vmc_config* c, int device,
       pct = std::max(1, std::min(100, pct));
       cudaFuncSetAttribute(P->kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
       cudaFuncSetAttribute(P->kern_trace, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      if (P->kern_solo) cudaFuncSetAttribute(P->kern_solo, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
       cudaGetLastError();
     }
   }
@@ -718,16 +725,20 @@ void plan_enqueue(vmc_plan* P, uint64_t first, uint64_t count, int64_t* d_cells,
   // faster on a less contended SM. Measured on B200 (profiles/README.md,
   // "small photon counts"): of 4 CTAs/SM, 2 are best below ~7 photons per
   // full-grid thread (B1 at 1e6: +19 %), 3 below ~30, all 4 above.
+  const void* kern = trace ? P->kern_trace : P->kern;
   if (!trace && P->grid_adaptive && full >= 4 * P->sms) {
     const int per = full / P->sms;
     const double r = static_cast<double>(count) / (static_cast<double>(full) * P->block);
     const int c = r < 7.0 ? per / 2 : (r < 30.0 ? per - per / 4 : per);
     full = c * P->sms;
+    // ... and the small-run instantiation (lane-local loop for a warp's last
+    // photon once the claims have run out); identical results
+    if (r < 30.0 && P->kern_solo) kern = P->kern_solo;
   }
   const int grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(full), std::max<uint64_t>(1, need_blocks)));
   {
     void* argv[] = {&A};
-    ck(cudaLaunchKernel(trace ? P->kern_trace : P->kern, dim3(grid), dim3(P->block), argv,
+    ck(cudaLaunchKernel(kern, dim3(grid), dim3(P->block), argv,
                         trace ? P->smem_trace : P->smem, st),
        "launch transport");
   }

@@ -148,7 +148,11 @@ struct FlightOps<double> {
 //               268-275,312-314, at CTA granularity). Ungated kernels only.
 // (kDepDirect / kDepWarp / kDepHotBox, kHotBoxN: transport.cuh)
 
-template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kDep = kDepDirect>
+// kSolo: the small-run instantiation (host: launches below ~30 photons per
+// full-grid thread). Once the claims have run out, a warp's last live photon
+// finishes in a lane-local loop (no votes, no event-phase dispatch); a
+// separate instantiation so the large-run kernel's code is untouched.
+template <typename Real, bool kGates, bool kDet, bool kTrace, bool kUni, int kDep = kDepDirect, bool kSolo = false>
 __device__ __forceinline__ void flight_body(const KernelArgs& A) {
   using Tr = RealTraits<Real>;
   using F = FlightOps<Real>;
@@ -957,6 +961,27 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     if (exhausted) {
       const unsigned dead = __ballot_sync(0xffffffffu, phase == DEAD);
       if (dead == 0xffffffffu) break;
+      if constexpr (kSolo) {
+        // the warp's last photon of a small run (typically a horizon-truncated
+        // one with hundreds of scatters left): nothing to batch with, so it
+        // runs to its end without votes or event-phase dispatch
+        if (__popc(dead) == 31) {
+          if (phase != DEAD) {
+            for (;;) {
+              if (phase == WALK) {
+                walk();
+                continue;
+              }
+              if (phase == ENDF) end_flight();
+              if (phase == SCAT || phase == RETRY) scatter();
+              if (phase == FACE) face();
+              if (phase == SETUP) setup();
+              if (phase == DEAD) break;
+            }
+          }
+          break;
+        }
+      }
       keep = ((32 - __popc(dead)) * A.walk_keep) >> 5;
     }
     // After an event phase nearly every lane walks in the cube60 kernels, so

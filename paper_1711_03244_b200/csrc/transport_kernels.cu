@@ -60,18 +60,26 @@ const void* VMC_CAT(transport_kernel_, VMC_REAL)(bool gates, bool det, bool trac
 
 // K1f (flight.cuh). FP32: the product kernel, same register cap as K1.
 // FP64 (--fmad=false): the exact-arithmetic pin of the same flight structure.
-template <typename R, bool G, bool D, bool T, bool U, int Dep = kDepDirect>
+template <typename R, bool G, bool D, bool T, bool U, int Dep = kDepDirect, bool Solo = false>
 __global__ void __launch_bounds__(kBlock, VMC_MIN_BLOCKS_PLAIN) k_flight(const __grid_constant__ KernelArgs A) {
-  flight_body<R, G, D, T, U, Dep>(A);
+  flight_body<R, G, D, T, U, Dep, Solo>(A);
 }
 
 #if VMC_REAL_IS_FLOAT
 // dep: deposit path (kDepDirect / kDepWarp / kDepHotBox, see flight.cuh); the
 // aggregated paths exist for the production variants of the BASELINE
 // workloads only (nullptr otherwise)
-const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep) {
+const void* flight_kernel_float(bool gates, bool det, bool trace, bool uniform, int dep, bool solo) {
   using R = float;
   const int key = (gates ? 4 : 0) | (det ? 2 : 0) | (trace ? 1 : 0);
+  if (solo) {  // small-run instantiations of the production variants (direct deposits)
+    if (dep != kDepDirect) return nullptr;
+    if (uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, kDepDirect, true>);
+    if (!uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, false, kDepDirect, true>);
+    if (!uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, kDepDirect, true>);
+    if (!uniform && key == 4) return reinterpret_cast<const void*>(&k_flight<R, true, false, false, false, kDepDirect, true>);
+    return nullptr;
+  }
   if (dep == kDepWarp) {
     if (uniform && key == 0) return reinterpret_cast<const void*>(&k_flight<R, false, false, false, true, kDepWarp>);
     if (!uniform && key == 2) return reinterpret_cast<const void*>(&k_flight<R, false, true, false, false, kDepWarp>);

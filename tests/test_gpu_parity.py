@@ -206,9 +206,10 @@ def test_map_replicas_bit_identical(gpu, monkeypatch, name):
                                     ("head", 50_000)])
 def test_small_run_scheduling_bit_identical(gpu, monkeypatch, name, n):
     """Small runs launch fewer resident CTAs per SM (2 or 3 of 4 below 7 / 30
-    photons per full-grid thread). Which lane carries a photon never changes
-    what it computes: maps, dispositions and detector records equal those of
-    the full grid."""
+    photons per full-grid thread) and the small-run instantiation of the kernel
+    (a warp's last photon finishes in a lane-local loop). Which lane carries a
+    photon, and in which loop, never changes what it computes: maps,
+    dispositions and detector records equal those of the full grid."""
     st = setup(name, n=n)
     runs = []
     for grid in ("0", "1"):
