@@ -63,15 +63,6 @@
 
 #include "transport.cuh"
 
-// Compile-time A/B knobs of the detector kernels (B3): walk steps per warp
-// vote, and whether the walk loop votes before its first pass.
-#ifndef VMC_WALK_STEPS_DET
-#define VMC_WALK_STEPS_DET 3  // 2 or 3
-#endif
-#ifndef VMC_VOTE_FIRST_DET
-#define VMC_VOTE_FIRST_DET 0
-#endif
-
 namespace vmc {
 
 #ifdef VMC_STATS
@@ -988,24 +979,21 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // their first vote is skipped (+1 %); in the strongly scattering head most
     // new flights end in their voxel, so the gated kernel votes first
     // (three steps per vote amortise the loop control; 2 and 4 measured slower)
-    constexpr int kSteps = kDet ? VMC_WALK_STEPS_DET : 3;
-    if constexpr (kGates || (kDet && VMC_VOTE_FIRST_DET)) {
+    // (written as three calls: a `#pragma unroll` loop of the same three
+    // calls changes the register allocation of the whole kernel, -7 %)
+    if constexpr (kGates) {
       while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep) {
         VMC_ST(6, 1);
         if (phase == WALK) walk();
         if (phase == WALK) walk();
-        if constexpr (kSteps >= 3) {
-          if (phase == WALK) walk();
-        }
+        if (phase == WALK) walk();
       }
     } else {
       do {
         VMC_ST(6, 1);
         if (phase == WALK) walk();
         if (phase == WALK) walk();
-        if constexpr (kSteps >= 3) {
-          if (phase == WALK) walk();
-        }
+        if (phase == WALK) walk();
       } while (__popc(__ballot_sync(0xffffffffu, phase == WALK)) > keep);
     }
   }
