@@ -539,8 +539,9 @@ class Plan:
 
 
 def demangle_kernel(mangled: str) -> str:
-    """_ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi0EEEvNS_10KernelArgsE -> k_flight<float,1,0,0,0,0>
-    (the two kernel templates' Itanium manglings, decoded without c++filt)."""
+    """_ZN3vmc8k_flightIfLb1ELb0ELb0ELb0ELi0ELb0EEEvNS_10KernelArgsE -> k_flight<float,1,0,0,0,0>
+    (the two kernel templates' Itanium manglings, decoded without c++filt; the
+    small-run instantiation of K1f shows its trailing kSolo = 1)."""
     import re
     m = re.match(r"_ZN3vmc(\d+)(k_flight|k_transport)I([fd])((?:L[bi]n?\d+E)+)E", mangled or "")
     if not m:
@@ -548,6 +549,8 @@ def demangle_kernel(mangled: str) -> str:
     args = ["float" if m.group(3) == "f" else "double"]
     for kind, neg, val in re.findall(r"L([bi])(n?)(\d+)E", m.group(4)):
         args.append(("-" if neg else "") + val)
+    if m.group(2) == "k_flight" and len(args) == 7 and args[-1] == "0":
+        args.pop()  # k_flight<..., kSolo = false>: the large-run kernel keeps its short name
     return f"{m.group(2)}<{','.join(args)}>"
 
 

@@ -128,3 +128,13 @@ def test_compute_fails_loudly_without_gpu():
         v.run_group_dynamic(0, 100, 1, st.scene, st.config)
     with pytest.raises(RuntimeError):
         v.rng_kat(1, 2, 3)
+
+
+def test_kernel_names_demangle():
+    """Plan.kernel names: the large-run K1f keeps k_flight<Real,G,D,T,U,Dep>, the
+    small-run instantiation shows its trailing kSolo = 1."""
+    from paper_1711_03244_b200.runtime import demangle_kernel as d
+    assert d("_ZN3vmc8k_flightIfLb0ELb1ELb0ELb0ELi0ELb0EEEvNS_10KernelArgsE") == "k_flight<float,0,1,0,0,0>"
+    assert d("_ZN3vmc8k_flightIfLb0ELb1ELb0ELb0ELi0ELb1EEEvNS_10KernelArgsE") == "k_flight<float,0,1,0,0,0,1>"
+    assert d("_ZN3vmc8k_flightIdLb1ELb0ELb0ELb1ELi0ELb0EEEvNS_10KernelArgsE") == "k_flight<double,1,0,0,1,0>"
+    assert d("_ZN3vmc11k_transportIfLb0ELb1ELb0ELb0EEEvNS_10KernelArgsE") == "k_transport<float,0,1,0,0>"
