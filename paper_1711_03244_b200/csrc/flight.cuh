@@ -924,11 +924,11 @@ __device__ __forceinline__ void flight_body(const KernelArgs& A) {
     // multi-label kernels: reconverge after the refill (+3 % B3, +1.5 % head;
     // the single-label kernel is ~0.4 % faster without)
     if constexpr (!kUni) __syncwarp();
-    // (lane-disjoint blocks: the order only moves code. Single-label kernels
-    // run the interface block first: B1 +2.2 %, B2 +2.0 %; the multi-label
-    // kernels keep scatter first: B3 -0.3 % the other way)
+    // (lane-disjoint blocks: the order only moves code. Single-label and gated
+    // kernels run the interface block first: B1 +2.2 %, B2 +2.0 %, head
+    // +0.25 %; the detector kernel keeps scatter first: B3 -0.3 % the other way)
     if (phase == ENDF) end_flight();
-    if constexpr (kUni) {
+    if constexpr (kUni || kGates) {
       if (phase == FACE) face();
       if (phase == SCAT || phase == RETRY) scatter();
     } else {
