@@ -236,8 +236,9 @@ struct PhotonDisposition {
 // ---- single-photon state and host helpers (reference transport.hpp:16-83) --
 // The walk itself runs on the device (simulate_photon below, the executors);
 // these scalar helpers give reference callers the same one-photon building
-// blocks (launch state, DDA distance, one HG deflection, one roulette draw) on
-// the host, e.g. for tests and diagnostics. They are not used by any executor.
+// blocks (launch state, DDA distance, one HG deflection, one walk segment,
+// one interface, one roulette draw) on the host, in the reference's double
+// arithmetic, e.g. for tests and diagnostics. They are not used by any executor.
 struct PhotonState {
   Vec3 position;
   Vec3 direction;
@@ -265,6 +266,9 @@ struct StepOutcome {
 PhotonState launch(const Source& source, const VoxelGrid& grid, RngStream& stream);
 double distance_to_voxel_boundary(const Vec3& position, const Vec3& direction, const VoxelGrid& grid);
 Vec3 hg_scatter(const Vec3& direction, double g, RngStream& stream);
+StepOutcome advance(PhotonState& photon, const VoxelGrid& grid, const SimulationConfig& config, RngStream& stream);
+StepOutcome handle_interface(PhotonState& photon, const VoxelGrid& grid, const SimulationConfig& config,
+                             const StepOutcome& crossing, RngStream& stream);
 bool roulette(PhotonState& photon, const SimulationConfig& config, RngStream& stream);
 
 // One photon's walk (reference transport.hpp:105-113), executed on CUDA device

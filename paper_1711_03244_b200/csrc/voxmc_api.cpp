@@ -236,21 +236,162 @@ PhotonState launch(const Source& source, const VoxelGrid& grid, RngStream& strea
   return st;
 }
 
+namespace {
+// Distance along the photon's direction to the nearest bounding plane of the
+// voxel `v` (the integer index is authoritative, transport.cpp:49-73): per axis
+// ((v + [d > 0]) h - p) / d clamped at 0, +inf for a zero component; `axis`
+// reports the plane's axis, ties going to the lower axis.
+double nearest_plane(const PhotonState& st, const VoxelIndex& v, double h, int& axis) {
+  const int iv[3] = {v.x, v.y, v.z};
+  double best = kInfD;
+  axis = 0;
+  for (int k = 0; k < 3; ++k) {
+    const double dk = st.direction[k];
+    if (dk == 0.0) continue;  // never crosses its planes
+    const double t = std::max(0.0, ((iv[k] + (dk > 0.0 ? 1 : 0)) * h - st.position[k]) * st.inv_direction[k]);
+    if (t < best) {  // strict: ties keep the lower axis
+      best = t;
+      axis = k;
+    }
+  }
+  return best;
+}
+
+// exp(-x) the way the reference evaluates it (transport.cpp:22-27): the
+// degree-4 series below 0.01, libm above
+double beer_lambert(double x) {
+  return x < 0.01 ? 1.0 - x * (1.0 - x * (0.5 - x * (1.0 / 6.0 - x * (1.0 / 24.0)))) : std::exp(-x);
+}
+
+// mirror the direction component of `axis` (specular reflection off that face)
+void mirror(PhotonState& photon, int axis) {
+  Vec3 d = photon.direction;
+  d.ref(axis) = -d[axis];
+  photon.set_direction(d);
+}
+}  // namespace
+
 double distance_to_voxel_boundary(const Vec3& position, const Vec3& direction, const VoxelGrid& grid) {
   const std::optional<VoxelIndex> v = grid.voxel_of(position);  // transport.cpp:108-118, :49-73
   if (!v) throw VoxelOutOfRange("position outside grid");
   PhotonState st;
   st.position = position;
   st.set_direction(direction);
-  const int iv[3] = {v->x, v->y, v->z};
-  double best = kInfD;
-  for (int k = 0; k < 3; ++k) {
-    if (direction[k] == 0.0) continue;  // a zero component never crosses its planes
-    const double plane = (iv[k] + (direction[k] > 0.0 ? 1 : 0)) * grid.voxel_size();
-    const double t = std::max(0.0, (plane - position[k]) * st.inv_direction[k]);
-    if (t < best) best = t;  // strict: ties keep the lower axis
+  int axis = 0;
+  return nearest_plane(st, *v, grid.voxel_size(), axis);
+}
+
+// One segment of the walk (transport.hpp:64-70, transport.cpp:161-225): the
+// photon moves to whichever comes first of its voxel's nearest face, its
+// scattering point and the time horizon, losing weight by Beer-Lambert on the
+// way (returned in `deposited`; the caller books it in the voxel it left).
+// A scattering point deflects it in place (HG + rejection azimuth) and draws
+// the next free path; the horizon truncates it; a face lands it exactly on
+// the plane and moves the voxel index, unless the next voxel is outside the
+// grid or has another refractive index (interface_pending for
+// handle_interface).
+StepOutcome advance(PhotonState& photon, const VoxelGrid& grid, const SimulationConfig& config, RngStream& stream) {
+  const OpticalProperties& m = grid.medium(photon.medium);
+  const double h = grid.voxel_size();
+  int axis = 0;
+  const double to_face = nearest_plane(photon, photon.voxel, h, axis);
+  const double to_scatter = m.mus > 0.0 ? photon.remaining_scat / m.mus : kInfD;
+  const double ns_per_mm = m.n * (1.0 / kLightSpeedMmPerNs);
+  const double time_left = config.tmax_ns - photon.time_ns;
+  const double first = std::min(to_face, to_scatter);
+  const bool horizon = first * ns_per_mm >= time_left;  // scatter / face lose ties to the horizon
+  const double d = horizon ? std::max(0.0, time_left / ns_per_mm) : first;
+
+  StepOutcome out;
+  const double w = photon.weight * beer_lambert(m.mua * d);
+  out.deposited = photon.weight - w;
+  photon.weight = w;
+  photon.time_ns += d * ns_per_mm;
+  if (horizon) {
+    photon.position = photon.position + photon.direction * d;
+    photon.time_ns = config.tmax_ns;
+    out.kind = StepKind::Terminated;
+    return out;
   }
-  return best;
+  if (to_scatter <= to_face) {  // the scattering point wins a tie with the face
+    photon.position = photon.position + photon.direction * d;
+    photon.set_direction(hg_scatter(photon.direction, m.g, stream));
+    photon.remaining_scat = unit_length(stream);
+    out.kind = StepKind::Scattered;
+    return out;
+  }
+  photon.remaining_scat = std::max(0.0, photon.remaining_scat - d * m.mus);
+  const int step = photon.direction[axis] > 0.0 ? 1 : -1;
+  Vec3 p = photon.position + photon.direction * d;
+  const int iv = axis == 0 ? photon.voxel.x : (axis == 1 ? photon.voxel.y : photon.voxel.z);
+  p.ref(axis) = (iv + (step > 0 ? 1 : 0)) * h;  // exactly on the crossed plane
+  photon.position = p;
+  VoxelIndex next = photon.voxel;
+  (axis == 0 ? next.x : (axis == 1 ? next.y : next.z)) += step;
+  out.kind = StepKind::CrossedVoxel;
+  out.face_axis = axis;
+  out.face_step = step;
+  out.next_voxel = next;
+  out.next_is_exterior = !grid.contains(next);
+  out.interface_pending = out.next_is_exterior || grid.medium_at(next).n != m.n;
+  if (!out.interface_pending) {
+    photon.voxel = next;
+    photon.medium = grid.label(next);
+  }
+  return out;
+}
+
+// A pending face from advance() (transport.hpp:72-79, transport.cpp:227-298):
+// leaves the grid at once in TerminateAtBoundary mode; otherwise an identity
+// index passes (or exits the grid) without a draw, total internal reflection
+// mirrors the normal component without a draw, and else one uniform against
+// the Fresnel reflectance picks mirror reflection or Snell refraction
+// (tangential components scaled by n1/n2, normal component ±cos t,
+// renormalised), after which the photon enters the next voxel or exits.
+StepOutcome handle_interface(PhotonState& photon, const VoxelGrid& grid, const SimulationConfig& config,
+                             const StepOutcome& crossing, RngStream& stream) {
+  StepOutcome out;
+  out.face_axis = crossing.face_axis;
+  out.face_step = crossing.face_step;
+  const bool outside = crossing.next_is_exterior;
+  auto enter_or_exit = [&]() {
+    if (outside) {
+      out.kind = StepKind::ExitedDomain;
+    } else {
+      photon.voxel = crossing.next_voxel;
+      photon.medium = grid.label(crossing.next_voxel);
+      out.kind = StepKind::CrossedVoxel;
+    }
+    return out;
+  };
+  if (outside && config.boundary_mode == BoundaryMode::TerminateAtBoundary) {
+    out.kind = StepKind::ExitedDomain;
+    return out;
+  }
+  const double n1 = grid.medium(photon.medium).n;
+  const double n2 = outside ? grid.exterior().n : grid.medium_at(crossing.next_voxel).n;
+  if (n1 == n2) return enter_or_exit();
+  const int axis = crossing.face_axis;
+  const double ci = std::fabs(photon.direction[axis]);
+  const double eta = n1 / n2;
+  const double st2 = eta * eta * std::max(0.0, 1.0 - ci * ci);
+  if (st2 > 1.0) {  // total internal reflection
+    mirror(photon, axis);
+    out.kind = StepKind::Reflected;
+    return out;
+  }
+  const double ct = std::sqrt(1.0 - st2);
+  const double rs = (n1 * ci - n2 * ct) / (n1 * ci + n2 * ct);
+  const double rp = (n1 * ct - n2 * ci) / (n1 * ct + n2 * ci);
+  if (stream.next_unit() < 0.5 * (rs * rs + rp * rp)) {
+    mirror(photon, axis);
+    out.kind = StepKind::Reflected;
+    return out;
+  }
+  Vec3 d = photon.direction * eta;
+  d.ref(axis) = photon.direction[axis] > 0.0 ? ct : -ct;
+  photon.set_direction(d.normalized());
+  return enter_or_exit();
 }
 
 Vec3 hg_scatter(const Vec3& direction, double g, RngStream& stream) {  // transport.cpp:126-147
