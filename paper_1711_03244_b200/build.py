@@ -24,6 +24,22 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
+
+def _json_include() -> str:
+    """nlohmann/json (the reference's own JSON dependency) as vendored in the
+    image (cudnn_frontend/thirdparty); VMC_JSON_INCLUDE overrides."""
+    env = os.environ.get("VMC_JSON_INCLUDE")
+    if env:
+        return env
+    import glob
+    import site
+    roots = list(site.getsitepackages()) + [os.path.dirname(os.path.dirname(os.__file__))]
+    for r in roots:
+        for hit in glob.glob(os.path.join(r, "**", "nlohmann", "json.hpp"), recursive=True):
+            return os.path.dirname(os.path.dirname(hit))
+    raise RuntimeError("nlohmann/json.hpp not found (set VMC_JSON_INCLUDE)")
+
+
 # (source, object, extra flags)
 UNITS = [
     ("transport_kernels.cu", "transport_f32.o", ["-DVMC_REAL=float", "-DVMC_REAL_IS_FLOAT=1"]),
@@ -31,6 +47,7 @@ UNITS = [
     ("capi.cu", "capi.o", []),
     ("partition.cpp", "partition.o", []),
     ("voxmc_api.cpp", "voxmc_api.o", []),
+    ("voxmc_config.cpp", "voxmc_config.o", None),  # flags resolved at build time (JSON include)
 ]
 
 HEADERS = ["transport.cuh", "flight.cuh", "rng.cuh", "partition.hpp"]
@@ -63,7 +80,8 @@ def _compile(src: str, obj: str, extra, verbose: bool) -> None:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
-    units = [u for u in UNITS if os.path.exists(os.path.join(CSRC, u[0]))]
+    units = [(src, obj, extra if extra is not None else ["-I", _json_include()])
+             for src, obj, extra in UNITS if os.path.exists(os.path.join(CSRC, src))]
     with cf.ThreadPoolExecutor(max_workers=len(units)) as ex:
         for f in [ex.submit(_compile, s, o, e, verbose) for s, o, e in units]:
             f.result()

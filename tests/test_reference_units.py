@@ -1,5 +1,5 @@
 """The reference's own doctest unit files (proj/tests/test_{rng,fluence,domain,
-scheduler,transport}.cpp), compiled UNMODIFIED against the B200 drop-in headers
+scheduler,transport,cli_io}.cpp), compiled UNMODIFIED against the B200 drop-in headers
 (include/voxmc) with the doctest stand-in tests/cpp/doctest.h and linked to
 libvoxmc_b200.so (recipe: oracle/Makefile `reftests`, built by
 __graft_entry__.build() where /root/reference exists; the binaries travel with
@@ -7,7 +7,11 @@ the repo snapshot). Host-side units run here; the executor cases of
 test_scheduler (run_group_dynamic / run_static_split / run_multi_device) and
 test_transport (simulate_photon_trace: Beer-Lambert, horizon, per-photon
 accounting to 1e-9, chord lengths to 1e-9, per-voxel path lengths against the
-ray-march oracle, reproducibility) run on the B200 with -m gpu."""
+ray-march oracle, reproducibility) and test_cli_io's run_pipeline case run on
+the B200 with -m gpu. test_cli_io holds the C++ front door (include/voxmc/
+config.hpp, volume_io.hpp): raw volume + checksummed sidecar, corrupted-volume
+detection, config presets / overrides / explicit scenes / diagnostics, device
+rosters, scene hash, calibration cache, the pipeline report."""
 import os
 import subprocess
 
@@ -65,5 +69,22 @@ def test_reference_scheduler_unit_on_gpu(gpu):
     dynamic == static raw cells, per-thread accounting, and the multi-device
     merge == single-device raw cells (test_scheduler.cpp:157-178, 246-264)."""
     rc, out = run_unit("test_scheduler")
+    assert rc == 0, out[-3000:]
+    assert " 0 failed" in out
+
+
+@pytest.mark.parametrize("filt", ["volume files", "corrupted volume", "benchmark preset config", "photon count defaults",
+                                  "explicit scene", "bad configs", "device rosters", "host device", "scene hash",
+                                  "calibration cache"])
+def test_reference_cli_io_host_cases(filt):
+    rc, out = run_unit("test_cli_io", filt)
+    assert rc == 0, out[-3000:]
+    assert "test cases: 0 " not in out
+
+
+@pytest.mark.gpu
+def test_reference_cli_io_unit_on_gpu(gpu):
+    """All of test_cli_io.cpp, run_pipeline on the B200."""
+    rc, out = run_unit("test_cli_io")
     assert rc == 0, out[-3000:]
     assert " 0 failed" in out
