@@ -1392,42 +1392,92 @@ int vmc_plan_trace(vmc_plan* plan, uint64_t first_index, uint64_t count, vmc_pho
   });
 }
 
+namespace {
+// vmc_simulate_photon is a per-photon call (reference callers loop over it, e.g.
+// acceptance.cpp's criterion 3: 1e6 calls), so its plan and buffers are kept
+// per device and reused while the scene and the config stay the same (key: the
+// label digest plus every other input byte); a call is then one launch, one
+// sync and four small copies instead of a plan build, allocations and frees.
+struct SimContext {
+  std::mutex mu;
+  uint64_t key = 0;
+  std::unique_ptr<vmc_plan> P;
+  DevBuf cells, totals, det, detn, tr, lc, lw, ln;
+};
+
+SimContext& sim_context(int device) {
+  static SimContext* ctx = new SimContext[64];  // never destroyed: no cudaFree after CUDA teardown
+  if (device < 0 || device >= 64) fail_validation("device index out of range");
+  return ctx[device];
+}
+
+uint64_t sim_key(const vmc_scene* s, const vmc_config* c, uint64_t labels) {
+  std::vector<unsigned char> b;
+  auto put = [&](const void* p, size_t n) {
+    const auto* q = static_cast<const unsigned char*>(p);
+    b.insert(b.end(), q, q + n);
+  };
+  put(&labels, sizeof labels);
+  const int32_t dims[4] = {s->nx, s->ny, s->nz, s->nmedia};
+  put(dims, sizeof dims);
+  put(&s->voxel_mm, sizeof s->voxel_mm);
+  put(s->media, sizeof(double) * 4 * static_cast<size_t>(std::max(0, s->nmedia)));
+  put(s->src_pos, sizeof s->src_pos);
+  put(s->src_dir, sizeof s->src_dir);
+  put(&s->isotropic, sizeof s->isotropic);
+  vmc_config cc = *c;
+  cc.det = nullptr;
+  put(&cc, sizeof cc);
+  if (c->ndet > 0 && c->det) put(c->det, sizeof(double) * 4 * static_cast<size_t>(c->ndet));
+  return vmc_fnv1a64(b.data(), b.size());
+}
+}  // namespace
+
 int vmc_simulate_photon(const vmc_scene* scene, const vmc_config* config, uint64_t photon_index, int device,
                         uint64_t max_deposits, int64_t* cells_out, double* dw_out, uint64_t* n_deposits,
                         double* disp_out) {
   return guarded([&] {
     if (max_deposits && (!cells_out || !dw_out)) fail_validation("simulate_photon: null deposit buffers");
+    LabelInfo li;
+    validate(scene, config, &li);
     vmc_config c = *config;
     c.precision = VMC_PRECISION_FP64;  // the reference's arithmetic (FP64 flight kernel)
     c.ngates = 1;
-    vmc_plan P;
-    plan_init(&P, scene, &c, device);
-    DevBuf cells, totals, det, detn, tr, lc, lw, ln;
-    cells.alloc(P.ncells * sizeof(int64_t), device);
-    totals.alloc(4 * sizeof(int64_t), device);
-    const uint64_t cap = c.ndet > 0 ? c.det_capacity : 0;
-    det.alloc(cap * P.rec_stride, device);
-    detn.alloc(sizeof(uint64_t), device);
-    tr.alloc(sizeof(vmc_photon_trace), device);
-    lc.alloc(max_deposits * sizeof(long long), device);
-    lw.alloc(max_deposits * sizeof(double), device);
-    ln.alloc(sizeof(unsigned long long), device);
-    ck(cudaMemset(ln.p, 0, sizeof(unsigned long long)), "zero log");
-    DepLog log{static_cast<long long*>(lc.p), static_cast<double*>(lw.p), static_cast<unsigned long long*>(ln.p),
-               max_deposits};
-    plan_enqueue(&P, photon_index, 1, static_cast<int64_t*>(cells.p), static_cast<int64_t*>(totals.p), det.p,
-                 static_cast<uint64_t*>(detn.p), nullptr, VMC_RUN_ZERO, true, static_cast<vmc_photon_trace*>(tr.p),
-                 &log);
-    ck(cudaDeviceSynchronize(), "simulate_photon");
-    check_launch_errors(&P);
+    SimContext& X = sim_context(device);
+    std::lock_guard<std::mutex> lock(X.mu);
+    const uint64_t key = sim_key(scene, &c, li.digest);
+    if (!X.P || X.key != key) {
+      X.P.reset();
+      auto P = std::make_unique<vmc_plan>();
+      plan_init(P.get(), scene, &c, device);
+      X.cells.ensure(P->ncells * sizeof(int64_t), device);
+      X.totals.ensure(4 * sizeof(int64_t), device);
+      X.det.ensure(std::max<uint64_t>(1, c.ndet > 0 ? c.det_capacity : 0) * P->rec_stride, device);
+      X.detn.ensure(sizeof(uint64_t), device);
+      X.tr.ensure(sizeof(vmc_photon_trace), device);
+      X.ln.ensure(sizeof(unsigned long long), device);
+      X.P = std::move(P);
+      X.key = key;
+    }
+    vmc_plan* P = X.P.get();
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    X.lc.ensure(std::max<uint64_t>(1, max_deposits) * sizeof(long long), device);
+    X.lw.ensure(std::max<uint64_t>(1, max_deposits) * sizeof(double), device);
+    ck(cudaMemsetAsync(X.ln.p, 0, sizeof(unsigned long long), nullptr), "zero log");
+    DepLog log{static_cast<long long*>(X.lc.p), static_cast<double*>(X.lw.p),
+               static_cast<unsigned long long*>(X.ln.p), max_deposits};
+    plan_enqueue(P, photon_index, 1, static_cast<int64_t*>(X.cells.p), static_cast<int64_t*>(X.totals.p), X.det.p,
+                 static_cast<uint64_t*>(X.detn.p), nullptr, VMC_RUN_ZERO, true,
+                 static_cast<vmc_photon_trace*>(X.tr.p), &log);
     vmc_photon_trace t;
-    ck(cudaMemcpy(&t, tr.p, sizeof t, cudaMemcpyDeviceToHost), "download trace");
     unsigned long long n = 0;
-    ck(cudaMemcpy(&n, ln.p, sizeof n, cudaMemcpyDeviceToHost), "download log count");
+    ck(cudaMemcpy(&t, X.tr.p, sizeof t, cudaMemcpyDeviceToHost), "download trace");
+    ck(cudaMemcpy(&n, X.ln.p, sizeof n, cudaMemcpyDeviceToHost), "download log count");
+    check_launch_errors(P);
     const uint64_t keep = std::min<uint64_t>(n, max_deposits);
     if (keep) {
-      ck(cudaMemcpy(cells_out, lc.p, keep * sizeof(long long), cudaMemcpyDeviceToHost), "download log");
-      ck(cudaMemcpy(dw_out, lw.p, keep * sizeof(double), cudaMemcpyDeviceToHost), "download log");
+      ck(cudaMemcpy(cells_out, X.lc.p, keep * sizeof(long long), cudaMemcpyDeviceToHost), "download log");
+      ck(cudaMemcpy(dw_out, X.lw.p, keep * sizeof(double), cudaMemcpyDeviceToHost), "download log");
     }
     if (n_deposits) *n_deposits = n;
     if (disp_out) {

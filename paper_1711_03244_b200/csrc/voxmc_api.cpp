@@ -64,7 +64,15 @@ struct Abi {
     c.roulette_multiplier = cfg.roulette_multiplier;
     c.workgroup_size = 0;
     c.ngates = cfg.ngates;
-    c.precision = cfg.precision == Precision::FP64 ? VMC_PRECISION_FP64 : VMC_PRECISION_FP32;
+    // VMC_DROPIN_PRECISION=fp64 runs every drop-in call in the reference's
+    // arithmetic (the FP64 kernels) whatever the config says: reference
+    // programs that compare a single-photon walk against an executor, like
+    // acceptance.cpp's criterion 3, then compare like with like
+    static const bool force_fp64 = [] {
+      const char* e = std::getenv("VMC_DROPIN_PRECISION");
+      return e && std::string(e) == "fp64";
+    }();
+    c.precision = (force_fp64 || cfg.precision == Precision::FP64) ? VMC_PRECISION_FP64 : VMC_PRECISION_FP32;
     for (const Detector& d : cfg.detectors) det.insert(det.end(), {d.position.x, d.position.y, d.position.z, d.radius});
     c.ndet = static_cast<int32_t>(cfg.detectors.size());
     c.det = det.empty() ? nullptr : det.data();
