@@ -1,5 +1,5 @@
 """The reference's own doctest unit files (proj/tests/test_{rng,fluence,domain,
-scheduler,transport,cli_io}.cpp), compiled UNMODIFIED against the B200 drop-in headers
+scheduler,transport,cli_io,oracles}.cpp), compiled UNMODIFIED against the B200 drop-in headers
 (include/voxmc) with the doctest stand-in tests/cpp/doctest.h and linked to
 libvoxmc_b200.so (recipe: oracle/Makefile `reftests`, built by
 __graft_entry__.build() where /root/reference exists; the binaries travel with
@@ -29,7 +29,7 @@ def run_unit(name, filt=None):
     return r.returncode, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("name", ["test_rng", "test_fluence", "test_domain"])
+@pytest.mark.parametrize("name", ["test_rng", "test_fluence", "test_domain", "test_oracles"])
 def test_reference_host_units(name):
     rc, out = run_unit(name)
     assert rc == 0, out[-3000:]
